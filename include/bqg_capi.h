@@ -1,0 +1,213 @@
+/*
+ * bqg_capi.h -- C ABI of the B200-native BiQGEMM library (libbiqgemm_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/core/include/biqgemm/, "proj/core"): every entry point
+ * below replaces one reference function, cited as file:line.  The C++ host
+ * library in include/biqgemm_b200/ re-presents the reference's C++ API
+ * (Matrix, BinaryPlane, KeyMatrix, PackedLinear, biqgemm, ...) on top of
+ * these calls; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "d_" pointers are device memory,
+ *     "h_" pointers are host memory.  All matrices are row-major.
+ *   - Device entry points are stream-ordered and asynchronous; `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every function returns a bqg_status; nothing throws across the ABI.
+ *     bqg_last_error_message() gives the per-thread detail text.  The C++
+ *     wrapper maps BQG_ERR_INVALID_ARGUMENT to std::invalid_argument and the
+ *     format codes to the reference's FormatError hierarchy
+ *     (model_io.hpp:14-32), exactly like the reference throws.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point returns BQG_ERR_NO_DEVICE.
+ *
+ * Data layouts: see paper_2005_09904_b200/csrc/kernels.h and DESIGN.md.
+ */
+#ifndef BQG_CAPI_H
+#define BQG_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BQG_ABI_VERSION 1
+
+typedef enum bqg_status {
+    BQG_OK = 0,
+    BQG_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    BQG_ERR_CUDA = 2,             /* a CUDA runtime call failed */
+    BQG_ERR_NO_DEVICE = 3,        /* no usable CUDA device (no CPU fallback) */
+    BQG_ERR_OUT_OF_MEMORY = 4,
+    BQG_ERR_FORMAT = 5,           /* reference: FormatError (model_io.hpp:14) */
+    BQG_ERR_BAD_MAGIC = 6,        /* reference: BadMagicError (model_io.hpp:18) */
+    BQG_ERR_BAD_VERSION = 7,      /* reference: BadVersionError (model_io.hpp:22) */
+    BQG_ERR_TRUNCATED = 8,        /* reference: TruncatedError (model_io.hpp:26) */
+    BQG_ERR_RANGE = 9,            /* reference: RangeError (model_io.hpp:30) */
+    BQG_ERR_IO = 10,              /* reference: std::runtime_error (model_io.cpp:169,175) */
+    BQG_ERR_WORKSPACE = 11        /* workspace too small */
+} bqg_status;
+
+/* LutLayout (lut.hpp:71) and LutBuilder (lut.hpp:73). */
+enum { BQG_LUT_TABLE_MAJOR = 0, BQG_LUT_KEY_MAJOR = 1 };
+enum { BQG_LUT_DP = 0, BQG_LUT_NAIVE = 1 };
+
+const char* bqg_status_string(int status);
+const char* bqg_last_error_message(void);
+int bqg_abi_version(void);
+
+/* ---------------------------------------------------------------- host-only
+ * (no GPU needed) */
+
+/* Matrix<float>::random_uniform / random_normal (matrix.hpp:63-79): libstdc++
+ * mt19937_64 + uniform_real_distribution<float>(lo, hi) /
+ * normal_distribution<float>(0, 1), row-major fill of rows*cols values. */
+int bqg_random_uniform_f32(float* h_out, size_t rows, size_t cols, uint64_t seed, float lo, float hi);
+int bqg_random_normal_f32(float* h_out, size_t rows, size_t cols, uint64_t seed);
+int bqg_random_uniform_f64(double* h_out, size_t rows, size_t cols, uint64_t seed, double lo, double hi);
+int bqg_random_normal_f64(double* h_out, size_t rows, size_t cols, uint64_t seed);
+
+/* plan_tiles (kernel.hpp:58-70).  On the GPU the TileShape does not change the
+ * result or the launch (the device planner sizes its own work units); it is
+ * kept for API fidelity and validated like the reference does. */
+int bqg_plan_tiles(size_t m, size_t groups, size_t b, unsigned mu, size_t budget_bytes,
+                   size_t entry_bytes, size_t* t_w, size_t* t_h);
+
+/* footprint (model_io.cpp:182-194): out[0..3] = weight, activation, output,
+ * alpha bytes. */
+int bqg_footprint(uint64_t m, uint64_t n, unsigned weight_bits, uint64_t batch,
+                  unsigned activation_bits, unsigned output_bits, uint64_t* out4);
+
+/* Exact op counters (kernel.hpp:23-36, laws at 179-180 and lut.hpp:62-68):
+ * out[0] lut_build_ops = (2^mu + mu - 1)*G*b (DP) or 2^mu*mu*G*b (naive),
+ * out[1] lookups = out[2] accumulate_ops = m*G*b*beta, out[3] fma_ops = 0. */
+int bqg_op_counters(size_t m, size_t n, size_t b, unsigned beta, unsigned mu, int builder,
+                    uint64_t* out4);
+
+/* Bytes of the tiled device key layout for beta planes (mu <= 8). */
+size_t bqg_tiled_key_bytes(size_t m, size_t n, unsigned beta, unsigned mu);
+
+/* BQGM model file (model_io.cpp:65-141, format README.md:88-108), host side.
+ * bqg_bqgm_parse validates exactly like load() (magic, version, dims, mu,
+ * per-plane alpha + keys with range check, no trailing bytes) and reports the
+ * header; with non-NULL outputs it also copies alpha (beta x m f32) and keys
+ * (beta x m x G, u8 if mu <= 8 else u16, i.e. the file's own payload). */
+int bqg_bqgm_parse(const uint8_t* h_bytes, size_t len, size_t* m, size_t* n, unsigned* beta,
+                   unsigned* mu, float* h_alpha, void* h_keys);
+/* save() from packed keys (rowmajor u8/u16 as above) and alpha. *len is the
+ * buffer size on entry and the file size on return; h_out may be NULL. */
+int bqg_bqgm_serialize(const void* h_keys, const float* h_alpha, size_t m, size_t n, unsigned beta,
+                       unsigned mu, uint8_t* h_out, size_t* len);
+
+/* ----------------------------------------------------------- device primitives */
+
+/* quantize_greedy<float> (quantize.hpp:27-58), bit-exact.
+ * d_w: m x n f32.  d_planes: beta x m x ceil(n/32) u32 (BinaryPlane words).
+ * d_alpha: beta x m f32.  Uses a temporary fp64 buffer of beta*m doubles. */
+int bqg_quantize_greedy_f32(const float* d_w, size_t m, size_t n, unsigned beta,
+                            uint32_t* d_planes, float* d_alpha, void* stream);
+
+/* pack_keys (packing.hpp:84-107), bit-exact, for one plane.
+ * d_plane: m x ceil(n/32) words.  d_keys: m x G, u8 (mu <= 8) or u16. */
+int bqg_pack_keys(const uint32_t* d_plane, size_t m, size_t n, unsigned mu, void* d_keys,
+                  void* stream);
+
+/* Row-major u8 keys of beta planes (beta x m x G) -> the fast path's tiled
+ * layout (bqg_tiled_key_bytes bytes).  mu <= 8 only. */
+int bqg_tile_keys(const uint8_t* d_keys, size_t m, size_t n, unsigned beta, unsigned mu,
+                  uint8_t* d_tiled, void* stream);
+
+/* build_lut_block (lut.hpp:109-154) for groups [g0, g0+count) of x
+ * (x_rows x b), in the reference's LutBlock layout (lut.hpp:90-97).
+ *   _f32: the fast path's bank-owned shared-memory builder (mu <= 8),
+ *         fp32, DP order; bit-exact with the DP evaluated in fp32.
+ *   _f64: the exact path's builder, fp64, bit-exact with the reference.
+ * builder must be BQG_LUT_DP (the naive builder is an oracle only).
+ * *ops (may be NULL) receives the reference's counted ops. */
+int bqg_build_lut_f32(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0,
+                      size_t count, int layout, int builder, float* d_entries, uint64_t* ops,
+                      void* stream);
+int bqg_build_lut_f64(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0,
+                      size_t count, int layout, int builder, double* d_entries, uint64_t* ops,
+                      void* stream);
+
+/* The BiQGEMM multiply, biqgemm (kernel.hpp:246-258) / biqgemm_plane
+ * (kernel.hpp:209-215 when d_alpha == NULL, alpha = 1):
+ *     y(r, c) = sum_i alpha_i[r] * sum_g LUT_g,c[key_i(r, g)]
+ * Fast path (mu <= 8): d_keys is the TILED layout (bqg_tile_keys); fused
+ *   LUT build -> query -> alpha epilogue; fp32 LUT, fp32 group sums, fp64
+ *   cross-block/plane epilogue.  Deterministic and grid-invariant.
+ *   Workspace: bqg_biqgemm_workspace_bytes(); must be zero-filled before the
+ *   first call (the kernel leaves it zeroed).  pdl != 0 launches with
+ *   programmatic stream serialization (overlaps the predecessor's tail).
+ * x_rows <= G*mu (rows beyond x_rows are zero; kernel.hpp:132-134). */
+size_t bqg_biqgemm_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu);
+int bqg_biqgemm_f32(const uint8_t* d_keys_tiled, const float* d_alpha, const float* d_x,
+                    size_t x_rows, float* d_y, size_t m, size_t n, size_t b, unsigned beta,
+                    unsigned mu, void* d_workspace, size_t workspace_bytes, int pdl, void* stream);
+
+/* Exact path: any mu in 1..16, any b; d_keys ROW-MAJOR (beta x m x G, u8 for
+ * mu <= 8 else u16); fp64 LUT and accumulation in the reference's order, so y
+ * is bit-identical to the reference.  Workspace from
+ * bqg_biqgemm_exact_workspace_bytes (no zero-fill requirement). */
+size_t bqg_biqgemm_exact_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu);
+int bqg_biqgemm_exact_f32(const void* d_keys, const float* d_alpha, const float* d_x, size_t x_rows,
+                          float* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                          void* d_workspace, size_t workspace_bytes, void* stream);
+int bqg_biqgemm_exact_f64(const void* d_keys, const double* d_alpha, const double* d_x,
+                          size_t x_rows, double* d_y, size_t m, size_t n, size_t b, unsigned beta,
+                          unsigned mu, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------ layer handle
+ * A device-resident PackedLinear<float> (kernel.hpp:217-241) with its
+ * workspace and a private stream: what the reference's callers hold. */
+typedef struct bqg_layer bqg_layer;
+
+typedef struct bqg_kernel_stats {
+    /* OpCounters (kernel.hpp:23-36), exact, computed analytically */
+    uint64_t lut_build_ops, lookups, accumulate_ops, fma_ops;
+    /* KernelStats phase seconds (kernel.hpp:41-46), CUDA-event timed:
+     * build+query = the fused kernel, replace = H2D of x + D2H of y */
+    double build_seconds, query_seconds, replace_seconds;
+} bqg_kernel_stats;
+
+/* quantize_greedy + pack_linear on the device from host weights W (m x n). */
+int bqg_layer_create_from_weights(const float* h_w, size_t m, size_t n, unsigned beta, unsigned mu,
+                                  bqg_layer** out);
+/* From device weights (no H2D). */
+int bqg_layer_create_from_device_weights(const float* d_w, size_t m, size_t n, unsigned beta,
+                                         unsigned mu, bqg_layer** out);
+/* From an already packed model (PackedLinear / a loaded BQGM payload):
+ * h_keys row-major beta x m x G (u8 if mu <= 8 else u16), h_alpha beta x m
+ * (NULL = plane mode, alpha = 1). */
+int bqg_layer_create_from_keys(const void* h_keys, const float* h_alpha, size_t m, size_t n,
+                               unsigned beta, unsigned mu, bqg_layer** out);
+/* load() (model_io.cpp:92-141) straight onto the device. */
+int bqg_layer_load_bqgm(const uint8_t* h_bytes, size_t len, bqg_layer** out);
+void bqg_layer_destroy(bqg_layer* layer);
+
+int bqg_layer_shape(const bqg_layer* layer, size_t* m, size_t* n, unsigned* beta, unsigned* mu);
+/* Download keys (row-major, u8/u16) and alpha; plane words too if non-NULL. */
+int bqg_layer_export(const bqg_layer* layer, void* h_keys, float* h_alpha, uint32_t* h_planes);
+/* Device views (for device-resident timing and the sharded driver). */
+const uint8_t* bqg_layer_device_tiled_keys(const bqg_layer* layer);
+const void* bqg_layer_device_keys(const bqg_layer* layer);
+const float* bqg_layer_device_alpha(const bqg_layer* layer);
+
+/* biqgemm(model, x) with HOST x (x_rows x b) and HOST y (m x b): H2D of x,
+ * the fused kernel, D2H of y, synchronised before return -- the reference
+ * call's contract.  exact != 0 selects the exact (fp64, bit-identical) path.
+ * stats (may be NULL) ACCUMULATES like KernelStats (kernel.hpp:197-202). */
+int bqg_layer_forward_host(bqg_layer* layer, const float* h_x, size_t x_rows, size_t b, float* h_y,
+                           int exact, bqg_kernel_stats* stats);
+/* Device-resident forward on a caller stream (no copies, no sync). */
+int bqg_layer_forward_device(bqg_layer* layer, const float* d_x, size_t x_rows, size_t b, float* d_y,
+                             int exact, int pdl, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BQG_CAPI_H */

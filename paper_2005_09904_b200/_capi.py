@@ -1,0 +1,163 @@
+"""ctypes binding of include/bqg_capi.h (libbiqgemm_b200.so).
+
+This is the same binding a Python caller of the reference's C++ API would
+add.  Loading fails loudly when the library has not been
+built: there is no Python or CPU fallback for any compute entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libbiqgemm_b200.so"
+
+BQG_OK = 0
+BQG_ERR_INVALID_ARGUMENT = 1
+BQG_ERR_CUDA = 2
+BQG_ERR_NO_DEVICE = 3
+BQG_ERR_OUT_OF_MEMORY = 4
+BQG_ERR_FORMAT = 5
+BQG_ERR_BAD_MAGIC = 6
+BQG_ERR_BAD_VERSION = 7
+BQG_ERR_TRUNCATED = 8
+BQG_ERR_RANGE = 9
+BQG_ERR_IO = 10
+BQG_ERR_WORKSPACE = 11
+
+LUT_TABLE_MAJOR = 0
+LUT_KEY_MAJOR = 1
+LUT_DP = 0
+LUT_NAIVE = 1
+
+sz = C.c_size_t
+u32 = C.c_uint
+u64 = C.c_uint64
+vp = C.c_void_p
+i32 = C.c_int
+f32 = C.c_float
+f64 = C.c_double
+P = C.POINTER
+
+
+class KernelStats(C.Structure):
+    """bqg_kernel_stats == OpCounters + KernelStats (kernel.hpp:23-46)."""
+
+    _fields_ = [
+        ("lut_build_ops", u64),
+        ("lookups", u64),
+        ("accumulate_ops", u64),
+        ("fma_ops", u64),
+        ("build_seconds", f64),
+        ("query_seconds", f64),
+        ("replace_seconds", f64),
+    ]
+
+
+# name -> (restype, argtypes).  Every symbol declared in include/bqg_capi.h.
+SIGNATURES = {
+    "bqg_status_string": (C.c_char_p, [i32]),
+    "bqg_last_error_message": (C.c_char_p, []),
+    "bqg_abi_version": (i32, []),
+    "bqg_random_uniform_f32": (i32, [vp, sz, sz, u64, f32, f32]),
+    "bqg_random_normal_f32": (i32, [vp, sz, sz, u64]),
+    "bqg_random_uniform_f64": (i32, [vp, sz, sz, u64, f64, f64]),
+    "bqg_random_normal_f64": (i32, [vp, sz, sz, u64]),
+    "bqg_plan_tiles": (i32, [sz, sz, sz, u32, sz, sz, P(sz), P(sz)]),
+    "bqg_footprint": (i32, [u64, u64, u32, u64, u32, u32, P(u64)]),
+    "bqg_op_counters": (i32, [sz, sz, sz, u32, u32, i32, P(u64)]),
+    "bqg_tiled_key_bytes": (sz, [sz, sz, u32, u32]),
+    "bqg_bqgm_parse": (i32, [vp, sz, P(sz), P(sz), P(u32), P(u32), vp, vp]),
+    "bqg_bqgm_serialize": (i32, [vp, vp, sz, sz, u32, u32, vp, P(sz)]),
+    "bqg_quantize_greedy_f32": (i32, [vp, sz, sz, u32, vp, vp, vp]),
+    "bqg_pack_keys": (i32, [vp, sz, sz, u32, vp, vp]),
+    "bqg_tile_keys": (i32, [vp, sz, sz, u32, u32, vp, vp]),
+    "bqg_build_lut_f32": (i32, [vp, sz, sz, u32, sz, sz, i32, i32, vp, P(u64), vp]),
+    "bqg_build_lut_f64": (i32, [vp, sz, sz, u32, sz, sz, i32, i32, vp, P(u64), vp]),
+    "bqg_biqgemm_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
+    "bqg_biqgemm_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
+    "bqg_biqgemm_exact_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
+    "bqg_biqgemm_exact_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),
+    "bqg_biqgemm_exact_f64": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),
+    "bqg_layer_create_from_weights": (i32, [vp, sz, sz, u32, u32, P(vp)]),
+    "bqg_layer_create_from_device_weights": (i32, [vp, sz, sz, u32, u32, P(vp)]),
+    "bqg_layer_create_from_keys": (i32, [vp, vp, sz, sz, u32, u32, P(vp)]),
+    "bqg_layer_load_bqgm": (i32, [vp, sz, P(vp)]),
+    "bqg_layer_destroy": (None, [vp]),
+    "bqg_layer_shape": (i32, [vp, P(sz), P(sz), P(u32), P(u32)]),
+    "bqg_layer_export": (i32, [vp, vp, vp, vp]),
+    "bqg_layer_device_tiled_keys": (vp, [vp]),
+    "bqg_layer_device_keys": (vp, [vp]),
+    "bqg_layer_device_alpha": (vp, [vp]),
+    "bqg_layer_forward_host": (i32, [vp, vp, sz, sz, vp, i32, P(KernelStats)]),
+    "bqg_layer_forward_device": (i32, [vp, vp, sz, sz, vp, i32, i32, vp]),
+}
+
+
+class BiqgemmError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[{status}] {message}")
+        self.status = status
+
+
+class InvalidArgument(BiqgemmError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class FormatError(BiqgemmError):
+    """biqgemm::FormatError (model_io.hpp:14)."""
+
+
+class BadMagicError(FormatError):
+    pass
+
+
+class BadVersionError(FormatError):
+    pass
+
+
+class TruncatedError(FormatError):
+    pass
+
+
+class RangeError(FormatError):
+    pass
+
+
+class NoDeviceError(BiqgemmError):
+    pass
+
+
+_EXC = {
+    BQG_ERR_INVALID_ARGUMENT: InvalidArgument,
+    BQG_ERR_FORMAT: FormatError,
+    BQG_ERR_BAD_MAGIC: BadMagicError,
+    BQG_ERR_BAD_VERSION: BadVersionError,
+    BQG_ERR_TRUNCATED: TruncatedError,
+    BQG_ERR_RANGE: RangeError,
+    BQG_ERR_NO_DEVICE: NoDeviceError,
+}
+
+
+def _load() -> C.CDLL:
+    if not _LIB_PATH.exists():
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -m paper_2005_09904_b200.build` "
+            "(there is no fallback implementation)"
+        )
+    lib = C.CDLL(str(_LIB_PATH), mode=os.RTLD_NOW | getattr(os, "RTLD_GLOBAL", 0))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+LIB_PATH = str(_LIB_PATH)
+
+
+def check(status: int) -> None:
+    if status != BQG_OK:
+        msg = lib.bqg_last_error_message().decode(errors="replace")
+        raise _EXC.get(status, BiqgemmError)(status, msg)

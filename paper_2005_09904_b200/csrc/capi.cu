@@ -1,0 +1,801 @@
+// capi.cu -- implementation of include/bqg_capi.h.
+//
+// Host-side validation mirrors the reference's exceptions one for one (the
+// reference file:line is given at each check); compute goes to the sm_100a
+// kernels in quantize.cu / biqgemm_fast.cu / biqgemm_exact.cu.  There is no
+// CPU compute path: without a CUDA device every compute entry point fails
+// with BQG_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/bqg_capi.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_msg;
+
+int set_err(int st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_msg = buf;
+    return st;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) {
+        return set_err(BQG_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    }
+    return set_err(BQG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define BQG_CUDA(call)                                        \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return cuda_err(_e, #call);    \
+    } while (0)
+
+int ensure_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return set_err(BQG_ERR_NO_DEVICE,
+                       "no usable CUDA device (%s); the library has no CPU fallback",
+                       e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+    }
+    return BQG_OK;
+}
+
+#define BQG_NEED_DEVICE()                    \
+    do {                                     \
+        int _s = ensure_device();            \
+        if (_s != BQG_OK) return _s;         \
+    } while (0)
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+size_t groups_of(size_t n, unsigned mu) { return (n + mu - 1) / mu; }
+
+int check_mu(unsigned mu, const char* who) {
+    // packing.hpp:85-87, lut.hpp:16-18: mu in [1, 16]
+    if (mu < 1 || mu > 16) return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: mu out of range [1,16]", who);
+    return BQG_OK;
+}
+
+int check_dims(size_t m, size_t n, const char* who) {
+    // matrix.hpp:23-25 / packing.hpp:28-31: dimensions must be nonzero
+    if (m == 0 || n == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: dimensions must be nonzero", who);
+    return BQG_OK;
+}
+
+int check_x(size_t x_rows, size_t b, size_t n, unsigned mu, const char* who) {
+    if (x_rows == 0 || b == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: x dimensions must be nonzero", who);
+    // kernel.hpp:132-134: the key matrix must cover x's rows
+    if (static_cast<size_t>(mu) * groups_of(n, mu) < x_rows)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: key matrix too narrow for input", who);
+    return BQG_OK;
+}
+
+template <typename T, typename Dist>
+int fill_random(T* out, size_t rows, size_t cols, uint64_t seed, Dist dist) {
+    if (!out) return set_err(BQG_ERR_INVALID_ARGUMENT, "random fill: null output");
+    if (rows == 0 || cols == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "Matrix: dimensions must be nonzero");
+    std::mt19937_64 rng(seed);
+    const size_t count = rows * cols;
+    for (size_t i = 0; i < count; ++i) out[i] = dist(rng);
+    return BQG_OK;
+}
+
+}  // namespace
+
+// ============================================================== status / misc
+
+extern "C" const char* bqg_status_string(int status) {
+    switch (status) {
+        case BQG_OK: return "ok";
+        case BQG_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case BQG_ERR_CUDA: return "CUDA error";
+        case BQG_ERR_NO_DEVICE: return "no CUDA device";
+        case BQG_ERR_OUT_OF_MEMORY: return "out of device memory";
+        case BQG_ERR_FORMAT: return "format error";
+        case BQG_ERR_BAD_MAGIC: return "bad magic";
+        case BQG_ERR_BAD_VERSION: return "bad version";
+        case BQG_ERR_TRUNCATED: return "truncated";
+        case BQG_ERR_RANGE: return "value out of range";
+        case BQG_ERR_IO: return "I/O error";
+        case BQG_ERR_WORKSPACE: return "workspace too small";
+        default: return "unknown status";
+    }
+}
+
+extern "C" const char* bqg_last_error_message(void) { return g_msg.c_str(); }
+
+extern "C" int bqg_abi_version(void) { return BQG_ABI_VERSION; }
+
+// ============================================================== host-only
+
+extern "C" int bqg_random_uniform_f32(float* out, size_t rows, size_t cols, uint64_t seed, float lo, float hi) {
+    return fill_random(out, rows, cols, seed, std::uniform_real_distribution<float>(lo, hi));
+}
+extern "C" int bqg_random_normal_f32(float* out, size_t rows, size_t cols, uint64_t seed) {
+    return fill_random(out, rows, cols, seed, std::normal_distribution<float>(0.0f, 1.0f));
+}
+extern "C" int bqg_random_uniform_f64(double* out, size_t rows, size_t cols, uint64_t seed, double lo, double hi) {
+    return fill_random(out, rows, cols, seed, std::uniform_real_distribution<double>(lo, hi));
+}
+extern "C" int bqg_random_normal_f64(double* out, size_t rows, size_t cols, uint64_t seed) {
+    return fill_random(out, rows, cols, seed, std::normal_distribution<double>(0.0, 1.0));
+}
+
+extern "C" int bqg_plan_tiles(size_t m, size_t groups, size_t b, unsigned mu, size_t budget, size_t entry_bytes,
+                              size_t* t_w, size_t* t_h) {
+    if (mu > 63) return set_err(BQG_ERR_INVALID_ARGUMENT, "plan_tiles: mu too large");
+    const size_t per_group = (size_t(1) << mu) * b * entry_bytes;
+    // kernel.hpp:62-64
+    if (per_group == 0 || budget < per_group)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "plan_tiles: budget below one group's tables");
+    const size_t tw = std::min(groups, budget / per_group);
+    if (tw == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "plan_tiles: zero groups");
+    const size_t th = std::clamp<size_t>(budget / (tw * sizeof(uint32_t)), 1, std::max<size_t>(m, 1));
+    if (t_w) *t_w = tw;
+    if (t_h) *t_h = th;
+    return BQG_OK;
+}
+
+extern "C" int bqg_footprint(uint64_t m, uint64_t n, unsigned bits, uint64_t batch, unsigned abits, unsigned obits,
+                             uint64_t* out) {
+    // model_io.cpp:185-187
+    if (bits == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "footprint: weight bits must be >= 1");
+    out[0] = (m * n * bits + 7) / 8;
+    out[1] = (n * batch * abits + 7) / 8;
+    out[2] = (m * batch * obits + 7) / 8;
+    out[3] = bits >= 32 ? 0 : uint64_t(4) * m * bits;
+    return BQG_OK;
+}
+
+extern "C" int bqg_op_counters(size_t m, size_t n, size_t b, unsigned beta, unsigned mu, int builder,
+                               uint64_t* out) {
+    int s = check_mu(mu, "op_counters");
+    if (s) return s;
+    const uint64_t G = groups_of(n, mu);
+    const uint64_t table = uint64_t(1) << mu;
+    out[0] = (builder == BQG_LUT_NAIVE ? table * mu : table + mu - 1) * G * b;
+    out[1] = uint64_t(m) * G * b * beta;
+    out[2] = out[1];
+    out[3] = 0;
+    return BQG_OK;
+}
+
+extern "C" size_t bqg_tiled_key_bytes(size_t m, size_t n, unsigned beta, unsigned mu) {
+    if (mu < 1 || mu > 8) return 0;
+    const size_t G = groups_of(n, mu);
+    return ((G + 31) / 32) * beta * ((m + 31) / 32) * 1024;
+}
+
+// ---- BQGM (model_io.cpp:65-141) ----
+
+namespace {
+
+constexpr uint8_t kMagic[4] = {'B', 'Q', 'G', 'M'};
+constexpr uint16_t kVersion = 1;
+
+struct Cursor {
+    const uint8_t* p;
+    size_t len, pos;
+    bool need(size_t k) const { return pos + k <= len; }
+};
+
+int truncated(const Cursor& c) {
+    return set_err(BQG_ERR_TRUNCATED, "model file truncated at offset %zu", c.pos);
+}
+
+}  // namespace
+
+extern "C" int bqg_bqgm_parse(const uint8_t* bytes, size_t len, size_t* m_out, size_t* n_out, unsigned* beta_out,
+                              unsigned* mu_out, float* alpha, void* keys) {
+    Cursor c{bytes, len, 0};
+    if (!c.need(4)) return truncated(c);
+    if (std::memcmp(bytes, kMagic, 4) != 0) return set_err(BQG_ERR_BAD_MAGIC, "bad magic, expected BQGM");
+    c.pos = 4;
+    if (!c.need(2)) return truncated(c);
+    const uint16_t version = uint16_t(bytes[4] | (uint16_t(bytes[5]) << 8));
+    c.pos = 6;
+    if (version != kVersion) return set_err(BQG_ERR_BAD_VERSION, "unsupported version %u", unsigned(version));
+    auto u32 = [&](uint32_t& v) {
+        if (!c.need(4)) return false;
+        v = 0;
+        for (int i = 0; i < 4; ++i) v |= uint32_t(bytes[c.pos + i]) << (8 * i);
+        c.pos += 4;
+        return true;
+    };
+    uint32_t m = 0, n = 0;
+    if (!u32(m)) return truncated(c);
+    if (!u32(n)) return truncated(c);
+    if (!c.need(1)) return truncated(c);
+    const unsigned beta = bytes[c.pos++];
+    if (!c.need(1)) return truncated(c);
+    const unsigned mu = bytes[c.pos++];
+    // model_io.cpp:108-113
+    if (m == 0 || n == 0 || beta == 0) return set_err(BQG_ERR_RANGE, "zero dimension in header");
+    if (mu < 1 || mu > 16) return set_err(BQG_ERR_RANGE, "mu out of range [1,16]");
+    const size_t G = groups_of(n, mu);
+    const uint32_t limit = 1u << mu;
+    const bool wide = mu > 8;
+    for (unsigned i = 0; i < beta; ++i) {
+        for (size_t r = 0; r < m; ++r) {
+            uint32_t bits;
+            if (!u32(bits)) return truncated(c);
+            if (alpha) std::memcpy(alpha + size_t(i) * m + r, &bits, 4);
+        }
+        const size_t count = size_t(m) * G;
+        for (size_t k = 0; k < count; ++k) {
+            uint32_t key;
+            if (wide) {
+                if (!c.need(2)) return truncated(c);
+                key = uint32_t(bytes[c.pos]) | (uint32_t(bytes[c.pos + 1]) << 8);
+                c.pos += 2;
+            } else {
+                if (!c.need(1)) return truncated(c);
+                key = bytes[c.pos++];
+            }
+            if (key >= limit) return set_err(BQG_ERR_RANGE, "key out of range for mu=%u", mu);
+            if (keys) {
+                if (wide) static_cast<uint16_t*>(keys)[size_t(i) * count + k] = uint16_t(key);
+                else static_cast<uint8_t*>(keys)[size_t(i) * count + k] = uint8_t(key);
+            }
+        }
+    }
+    // model_io.cpp:137-139
+    if (c.pos != len) return set_err(BQG_ERR_FORMAT, "trailing bytes after payload");
+    *m_out = m;
+    *n_out = n;
+    *beta_out = beta;
+    *mu_out = mu;
+    return BQG_OK;
+}
+
+extern "C" int bqg_bqgm_serialize(const void* keys, const float* alpha, size_t m, size_t n, unsigned beta,
+                                  unsigned mu, uint8_t* out, size_t* len) {
+    int s = check_mu(mu, "save");  // model_io.cpp:66-68
+    if (s) return s;
+    if (m == 0 || n == 0 || beta == 0 || beta > 255 || m > 0xffffffffu || n > 0xffffffffu)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "save: dimensions out of range");
+    const size_t G = groups_of(n, mu);
+    const bool wide = mu > 8;
+    const size_t total = 16 + size_t(beta) * (4 * m + m * G * (wide ? 2 : 1));
+    if (out) {
+        if (*len < total) return set_err(BQG_ERR_INVALID_ARGUMENT, "save: buffer too small");
+        size_t pos = 0;
+        std::memcpy(out, kMagic, 4);
+        pos = 4;
+        out[pos++] = uint8_t(kVersion & 0xff);
+        out[pos++] = uint8_t(kVersion >> 8);
+        for (int i = 0; i < 4; ++i) out[pos++] = uint8_t(uint32_t(m) >> (8 * i));
+        for (int i = 0; i < 4; ++i) out[pos++] = uint8_t(uint32_t(n) >> (8 * i));
+        out[pos++] = uint8_t(beta);
+        out[pos++] = uint8_t(mu);
+        for (unsigned i = 0; i < beta; ++i) {
+            for (size_t r = 0; r < m; ++r) {
+                const float a = alpha ? alpha[size_t(i) * m + r] : 1.0f;
+                uint32_t bits;
+                std::memcpy(&bits, &a, 4);
+                for (int k = 0; k < 4; ++k) out[pos++] = uint8_t(bits >> (8 * k));
+            }
+            const size_t count = m * G;
+            for (size_t k = 0; k < count; ++k) {
+                if (wide) {
+                    const uint16_t v = static_cast<const uint16_t*>(keys)[size_t(i) * count + k];
+                    out[pos++] = uint8_t(v & 0xff);
+                    out[pos++] = uint8_t(v >> 8);
+                } else {
+                    out[pos++] = static_cast<const uint8_t*>(keys)[size_t(i) * count + k];
+                }
+            }
+        }
+    }
+    *len = total;
+    return BQG_OK;
+}
+
+// ============================================================== device primitives
+
+extern "C" int bqg_quantize_greedy_f32(const float* d_w, size_t m, size_t n, unsigned beta, uint32_t* d_planes,
+                                       float* d_alpha, void* stream) {
+    // quantize.hpp:29-31
+    if (beta == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "quantize_greedy: beta must be >= 1");
+    int s = check_dims(m, n, "quantize_greedy");
+    if (s) return s;
+    if (!d_w || !d_planes || !d_alpha) return set_err(BQG_ERR_INVALID_ARGUMENT, "quantize_greedy: null pointer");
+    BQG_NEED_DEVICE();
+    cudaStream_t st = as_stream(stream);
+    double* alpha_d = nullptr;
+    BQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&alpha_d), sizeof(double) * beta * m, st));
+    cudaError_t e = bqg::launch_quantize_greedy(d_w, static_cast<long long>(m), static_cast<long long>(n),
+                                                static_cast<int>(beta), d_planes, d_alpha, alpha_d, st);
+    cudaFreeAsync(alpha_d, st);
+    if (e != cudaSuccess) return cuda_err(e, "quantize_greedy kernel");
+    return BQG_OK;
+}
+
+extern "C" int bqg_pack_keys(const uint32_t* d_plane, size_t m, size_t n, unsigned mu, void* d_keys, void* stream) {
+    int s = check_mu(mu, "pack_keys");
+    if (s) return s;
+    s = check_dims(m, n, "pack_keys");
+    if (s) return s;
+    if (!d_plane || !d_keys) return set_err(BQG_ERR_INVALID_ARGUMENT, "pack_keys: null pointer");
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_pack_keys(d_plane, static_cast<long long>(m), static_cast<long long>(n),
+                                          static_cast<int>(mu), d_keys, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "pack_keys kernel");
+    return BQG_OK;
+}
+
+extern "C" int bqg_tile_keys(const uint8_t* d_keys, size_t m, size_t n, unsigned beta, unsigned mu,
+                             uint8_t* d_tiled, void* stream) {
+    if (mu < 1 || mu > 8) return set_err(BQG_ERR_INVALID_ARGUMENT, "tile_keys: tiled layout needs mu in [1,8]");
+    int s = check_dims(m, n, "tile_keys");
+    if (s) return s;
+    if (beta == 0 || !d_keys || !d_tiled) return set_err(BQG_ERR_INVALID_ARGUMENT, "tile_keys: bad argument");
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_tile_keys(d_keys, static_cast<long long>(m),
+                                          static_cast<long long>(groups_of(n, mu)), static_cast<int>(beta),
+                                          d_tiled, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "tile_keys kernel");
+    return BQG_OK;
+}
+
+namespace {
+int check_lut_args(size_t x_rows, size_t b, unsigned mu, size_t count, int layout, int builder, const char* who) {
+    int s = check_mu(mu, who);
+    if (s) return s;
+    if (count == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "build_lut_block: empty tile");  // lut.hpp:114-116
+    if (x_rows == 0 || b == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: x dimensions must be nonzero", who);
+    if (layout != BQG_LUT_TABLE_MAJOR && layout != BQG_LUT_KEY_MAJOR)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: unknown layout", who);
+    if (builder != BQG_LUT_DP)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: only the DP builder runs on the device", who);
+    return BQG_OK;
+}
+}  // namespace
+
+extern "C" int bqg_build_lut_f32(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0, size_t count,
+                                 int layout, int builder, float* d_entries, uint64_t* ops, void* stream) {
+    int s = check_lut_args(x_rows, b, mu, count, layout, builder, "build_lut_f32");
+    if (s) return s;
+    if (mu > 8) return set_err(BQG_ERR_INVALID_ARGUMENT, "build_lut_f32: shared-memory builder needs mu <= 8");
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_build_lut_f32(d_x, static_cast<long long>(x_rows), static_cast<long long>(b),
+                                              static_cast<int>(mu), static_cast<long long>(g0),
+                                              static_cast<long long>(count), layout == BQG_LUT_KEY_MAJOR,
+                                              d_entries, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "build_lut_f32 kernel");
+    if (ops) *ops += ((uint64_t(1) << mu) + mu - 1) * count * b;
+    return BQG_OK;
+}
+
+extern "C" int bqg_build_lut_f64(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0, size_t count,
+                                 int layout, int builder, double* d_entries, uint64_t* ops, void* stream) {
+    int s = check_lut_args(x_rows, b, mu, count, layout, builder, "build_lut_f64");
+    if (s) return s;
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_build_lut_exact<float>(
+        d_x, static_cast<long long>(x_rows), static_cast<long long>(b), static_cast<int>(mu),
+        static_cast<long long>(g0), static_cast<long long>(count), layout == BQG_LUT_KEY_MAJOR, d_entries,
+        as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "build_lut_f64 kernel");
+    if (ops) *ops += ((uint64_t(1) << mu) + mu - 1) * count * b;
+    return BQG_OK;
+}
+
+extern "C" size_t bqg_biqgemm_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu) {
+    if (mu < 1 || mu > 8 || m == 0 || n == 0 || b == 0 || beta == 0) return 0;
+    return bqg::fast_workspace_bytes(static_cast<long long>(m), static_cast<long long>(groups_of(n, mu)),
+                                     static_cast<int>(beta), static_cast<long long>(b));
+}
+
+namespace {
+bqg::QueryParams make_params(const uint8_t* keys, const float* alpha, const float* x, size_t x_rows, float* y,
+                             size_t m, size_t n, size_t b, unsigned beta, unsigned mu, void* ws) {
+    bqg::QueryParams p{};
+    const long long G = static_cast<long long>(groups_of(n, mu));
+    const long long MT = (static_cast<long long>(m) + 31) / 32;
+    const long long NB = (G + 31) / 32;
+    const int BT = b == 1 ? 1 : (b == 2 ? 2 : 4);
+    const long long CT = (static_cast<long long>(b) + BT - 1) / BT;
+    const size_t ctr_bytes = ((static_cast<size_t>(MT * CT) * sizeof(unsigned) + 255) / 256) * 256;
+    p.keys = keys;
+    p.alpha = alpha;
+    p.x = x;
+    p.y = y;
+    p.counters = static_cast<unsigned*>(ws);
+    p.partial = reinterpret_cast<float*>(static_cast<char*>(ws) + ctr_bytes);
+    p.x_rows = static_cast<long long>(x_rows);
+    p.m = static_cast<int>(m);
+    p.G = static_cast<int>(G);
+    p.NB = static_cast<int>(NB);
+    p.MT = static_cast<int>(MT);
+    p.beta = static_cast<int>(beta);
+    p.b = static_cast<int>(b);
+    p.cpb = 1;
+    return p;
+}
+}  // namespace
+
+extern "C" int bqg_biqgemm_f32(const uint8_t* d_keys, const float* d_alpha, const float* d_x, size_t x_rows,
+                               float* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu, void* d_ws,
+                               size_t ws_bytes, int pdl, void* stream) {
+    int s = check_mu(mu, "biqgemm");
+    if (s) return s;
+    if (mu > 8) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_f32: fast path needs mu <= 8 (use the exact path)");
+    s = check_dims(m, n, "biqgemm");
+    if (s) return s;
+    if (beta == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: beta must be >= 1");
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    if (m > 0x7fffffff || b > 0x7fffffff) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: dimension too large");
+    if (!d_keys || !d_x || !d_y || !d_ws) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null pointer");
+    if (ws_bytes < bqg_biqgemm_workspace_bytes(m, n, b, beta, mu))
+        return set_err(BQG_ERR_WORKSPACE, "biqgemm: workspace %zu < %zu bytes", ws_bytes,
+                       bqg_biqgemm_workspace_bytes(m, n, b, beta, mu));
+    BQG_NEED_DEVICE();
+    const bqg::QueryParams p = make_params(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, d_ws);
+    cudaError_t e = bqg::launch_biqgemm_fast(p, static_cast<int>(mu), pdl != 0, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "biqgemm fast kernel");
+    return BQG_OK;
+}
+
+extern "C" size_t bqg_biqgemm_exact_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu) {
+    if (mu < 1 || mu > 16 || m == 0 || n == 0 || b == 0 || beta == 0) return 0;
+    return bqg::exact_workspace_bytes(static_cast<long long>(m), static_cast<long long>(n), static_cast<int>(beta),
+                                      static_cast<int>(mu), static_cast<long long>(b));
+}
+
+template <typename T>
+static int biqgemm_exact_impl(const void* d_keys, const T* d_alpha, const T* d_x, size_t x_rows, T* d_y, size_t m,
+                              size_t n, size_t b, unsigned beta, unsigned mu, void* d_ws, size_t ws_bytes,
+                              void* stream) {
+    int s = check_mu(mu, "biqgemm");
+    if (s) return s;
+    s = check_dims(m, n, "biqgemm");
+    if (s) return s;
+    if (beta == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: beta must be >= 1");
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    if (!d_keys || !d_x || !d_y || !d_ws) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null pointer");
+    if (ws_bytes < bqg_biqgemm_exact_workspace_bytes(m, n, b, beta, mu))
+        return set_err(BQG_ERR_WORKSPACE, "biqgemm_exact: workspace too small");
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_biqgemm_exact<T>(d_keys, d_alpha, d_x, static_cast<long long>(x_rows), d_y,
+                                                 static_cast<long long>(m), static_cast<long long>(n),
+                                                 static_cast<int>(beta), static_cast<int>(mu),
+                                                 static_cast<long long>(b), d_ws, ws_bytes, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "biqgemm exact kernels");
+    return BQG_OK;
+}
+
+extern "C" int bqg_biqgemm_exact_f32(const void* d_keys, const float* d_alpha, const float* d_x, size_t x_rows,
+                                     float* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                     void* d_ws, size_t ws_bytes, void* stream) {
+    return biqgemm_exact_impl<float>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, d_ws, ws_bytes, stream);
+}
+
+extern "C" int bqg_biqgemm_exact_f64(const void* d_keys, const double* d_alpha, const double* d_x, size_t x_rows,
+                                     double* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                     void* d_ws, size_t ws_bytes, void* stream) {
+    return biqgemm_exact_impl<double>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, d_ws, ws_bytes, stream);
+}
+
+// ============================================================== layer handle
+
+struct bqg_layer {
+    size_t m = 0, n = 0, G = 0;
+    unsigned beta = 0, mu = 0;
+    bool plane_mode = false;
+    cudaStream_t stream = nullptr;
+    uint32_t* d_planes = nullptr;  // only when created from weights
+    void* d_keys = nullptr;        // row-major u8/u16
+    uint8_t* d_tiled = nullptr;    // mu <= 8
+    float* d_alpha = nullptr;
+    // forward scratch (grown on demand)
+    void* d_ws = nullptr;
+    size_t ws_bytes = 0;
+    void* d_ws_exact = nullptr;
+    size_t ws_exact_bytes = 0;
+    float* d_x = nullptr;
+    size_t x_cap = 0;
+    float* d_y = nullptr;
+    size_t y_cap = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::mutex mu_lock;
+
+    size_t key_bytes_per_plane() const { return m * G * (mu > 8 ? 2 : 1); }
+};
+
+namespace {
+
+void layer_free(bqg_layer* L) {
+    if (!L) return;
+    if (L->stream) cudaStreamSynchronize(L->stream);
+    cudaFree(L->d_planes);
+    cudaFree(L->d_keys);
+    cudaFree(L->d_tiled);
+    cudaFree(L->d_alpha);
+    cudaFree(L->d_ws);
+    cudaFree(L->d_ws_exact);
+    cudaFree(L->d_x);
+    cudaFree(L->d_y);
+    for (auto& e : L->ev)
+        if (e) cudaEventDestroy(e);
+    if (L->stream) cudaStreamDestroy(L->stream);
+    delete L;
+}
+
+int layer_alloc(size_t m, size_t n, unsigned beta, unsigned mu, bool plane_mode, bqg_layer** out) {
+    if (!out) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null output");
+    int s = check_mu(mu, "pack_linear");
+    if (s) return s;
+    s = check_dims(m, n, "pack_linear");
+    if (s) return s;
+    if (beta == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "quantize_greedy: beta must be >= 1");
+    if (m > 0x7fffffff) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: m too large");
+    BQG_NEED_DEVICE();
+    bqg_layer* L = new (std::nothrow) bqg_layer();
+    if (!L) return set_err(BQG_ERR_OUT_OF_MEMORY, "layer: host allocation failed");
+    L->m = m;
+    L->n = n;
+    L->beta = beta;
+    L->mu = mu;
+    L->G = groups_of(n, mu);
+    L->plane_mode = plane_mode;
+    cudaError_t e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&L->d_keys, L->key_bytes_per_plane() * beta);
+    if (e == cudaSuccess && mu <= 8) e = cudaMalloc(reinterpret_cast<void**>(&L->d_tiled), bqg_tiled_key_bytes(m, n, beta, mu));
+    if (e == cudaSuccess && !plane_mode) e = cudaMalloc(reinterpret_cast<void**>(&L->d_alpha), sizeof(float) * beta * m);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&L->ev[i]);
+    if (e != cudaSuccess) {
+        layer_free(L);
+        return cuda_err(e, "layer allocation");
+    }
+    *out = L;
+    return BQG_OK;
+}
+
+int layer_finish_tiling(bqg_layer* L) {
+    if (L->mu <= 8) {
+        cudaError_t e = bqg::launch_tile_keys(static_cast<const uint8_t*>(L->d_keys), static_cast<long long>(L->m),
+                                              static_cast<long long>(L->G), static_cast<int>(L->beta), L->d_tiled,
+                                              L->stream);
+        if (e != cudaSuccess) return cuda_err(e, "tile_keys kernel");
+    }
+    BQG_CUDA(cudaStreamSynchronize(L->stream));
+    return BQG_OK;
+}
+
+int layer_from_device_weights(const float* d_w, size_t m, size_t n, unsigned beta, unsigned mu, bqg_layer* L) {
+    const size_t wpr = (n + 31) / 32;
+    BQG_CUDA(cudaMalloc(reinterpret_cast<void**>(&L->d_planes), sizeof(uint32_t) * beta * m * wpr));
+    int s = bqg_quantize_greedy_f32(d_w, m, n, beta, L->d_planes, L->d_alpha, L->stream);
+    if (s) return s;
+    for (unsigned i = 0; i < beta; ++i) {
+        s = bqg_pack_keys(L->d_planes + size_t(i) * m * wpr, m, n, mu,
+                          static_cast<char*>(L->d_keys) + L->key_bytes_per_plane() * i, L->stream);
+        if (s) return s;
+    }
+    return layer_finish_tiling(L);
+}
+
+template <typename P>
+int grow(P*& ptr, size_t& cap, size_t need) {
+    if (need <= cap) return BQG_OK;
+    cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    BQG_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), need));
+    cap = need;
+    return BQG_OK;
+}
+
+}  // namespace
+
+extern "C" int bqg_layer_create_from_device_weights(const float* d_w, size_t m, size_t n, unsigned beta, unsigned mu,
+                                                    bqg_layer** out) {
+    bqg_layer* L = nullptr;
+    int s = layer_alloc(m, n, beta, mu, false, &L);
+    if (s) return s;
+    s = layer_from_device_weights(d_w, m, n, beta, mu, L);
+    if (s) {
+        layer_free(L);
+        return s;
+    }
+    *out = L;
+    return BQG_OK;
+}
+
+extern "C" int bqg_layer_create_from_weights(const float* h_w, size_t m, size_t n, unsigned beta, unsigned mu,
+                                             bqg_layer** out) {
+    if (!h_w) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null weights");
+    bqg_layer* L = nullptr;
+    int s = layer_alloc(m, n, beta, mu, false, &L);
+    if (s) return s;
+    float* d_w = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d_w), sizeof(float) * m * n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_w, h_w, sizeof(float) * m * n, cudaMemcpyHostToDevice, L->stream);
+    if (e != cudaSuccess) {
+        cudaFree(d_w);
+        layer_free(L);
+        return cuda_err(e, "layer weights upload");
+    }
+    s = layer_from_device_weights(d_w, m, n, beta, mu, L);
+    cudaStreamSynchronize(L->stream);
+    cudaFree(d_w);
+    if (s) {
+        layer_free(L);
+        return s;
+    }
+    *out = L;
+    return BQG_OK;
+}
+
+extern "C" int bqg_layer_create_from_keys(const void* h_keys, const float* h_alpha, size_t m, size_t n,
+                                          unsigned beta, unsigned mu, bqg_layer** out) {
+    if (!h_keys) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null keys");
+    {
+        int s = check_mu(mu, "pack_linear");
+        if (s) return s;
+    }
+    // Keys index 2^mu-entry tables: reject out-of-range keys up front
+    // (model_io.cpp:130-132 does the same for loaded files).
+    const size_t G = groups_of(n, mu);
+    const size_t count = size_t(beta) * m * G;
+    const uint32_t limit = 1u << mu;
+    for (size_t k = 0; k < count; ++k) {
+        const uint32_t v = mu > 8 ? static_cast<const uint16_t*>(h_keys)[k] : static_cast<const uint8_t*>(h_keys)[k];
+        if (v >= limit) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: key %u out of range for mu=%u", v, mu);
+    }
+    bqg_layer* L = nullptr;
+    int s = layer_alloc(m, n, beta, mu, h_alpha == nullptr, &L);
+    if (s) return s;
+    cudaError_t e = cudaMemcpyAsync(L->d_keys, h_keys, L->key_bytes_per_plane() * beta, cudaMemcpyHostToDevice,
+                                    L->stream);
+    if (e == cudaSuccess && h_alpha)
+        e = cudaMemcpyAsync(L->d_alpha, h_alpha, sizeof(float) * beta * m, cudaMemcpyHostToDevice, L->stream);
+    if (e != cudaSuccess) {
+        layer_free(L);
+        return cuda_err(e, "layer upload");
+    }
+    s = layer_finish_tiling(L);
+    if (s) {
+        layer_free(L);
+        return s;
+    }
+    *out = L;
+    return BQG_OK;
+}
+
+extern "C" int bqg_layer_load_bqgm(const uint8_t* bytes, size_t len, bqg_layer** out) {
+    size_t m, n;
+    unsigned beta, mu;
+    int s = bqg_bqgm_parse(bytes, len, &m, &n, &beta, &mu, nullptr, nullptr);
+    if (s) return s;
+    const size_t G = groups_of(n, mu);
+    std::vector<float> alpha(size_t(beta) * m);
+    std::vector<uint8_t> keys(size_t(beta) * m * G * (mu > 8 ? 2 : 1));
+    s = bqg_bqgm_parse(bytes, len, &m, &n, &beta, &mu, alpha.data(), keys.data());
+    if (s) return s;
+    return bqg_layer_create_from_keys(keys.data(), alpha.data(), m, n, beta, mu, out);
+}
+
+extern "C" void bqg_layer_destroy(bqg_layer* layer) { layer_free(layer); }
+
+extern "C" int bqg_layer_shape(const bqg_layer* L, size_t* m, size_t* n, unsigned* beta, unsigned* mu) {
+    if (!L) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null");
+    if (m) *m = L->m;
+    if (n) *n = L->n;
+    if (beta) *beta = L->beta;
+    if (mu) *mu = L->mu;
+    return BQG_OK;
+}
+
+extern "C" int bqg_layer_export(const bqg_layer* L, void* h_keys, float* h_alpha, uint32_t* h_planes) {
+    if (!L) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null");
+    if (h_keys) BQG_CUDA(cudaMemcpy(h_keys, L->d_keys, L->key_bytes_per_plane() * L->beta, cudaMemcpyDeviceToHost));
+    if (h_alpha) {
+        if (L->d_alpha) {
+            BQG_CUDA(cudaMemcpy(h_alpha, L->d_alpha, sizeof(float) * L->beta * L->m, cudaMemcpyDeviceToHost));
+        } else {
+            for (size_t i = 0; i < size_t(L->beta) * L->m; ++i) h_alpha[i] = 1.0f;
+        }
+    }
+    if (h_planes) {
+        if (!L->d_planes) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: no sign planes (created from keys)");
+        BQG_CUDA(cudaMemcpy(h_planes, L->d_planes, sizeof(uint32_t) * L->beta * L->m * ((L->n + 31) / 32),
+                            cudaMemcpyDeviceToHost));
+    }
+    return BQG_OK;
+}
+
+extern "C" const uint8_t* bqg_layer_device_tiled_keys(const bqg_layer* L) { return L ? L->d_tiled : nullptr; }
+extern "C" const void* bqg_layer_device_keys(const bqg_layer* L) { return L ? L->d_keys : nullptr; }
+extern "C" const float* bqg_layer_device_alpha(const bqg_layer* L) { return L ? L->d_alpha : nullptr; }
+
+namespace {
+
+int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float* d_y, int exact, int pdl,
+                  cudaStream_t st) {
+    if (exact || L->mu > 8) {
+        const size_t need = bqg_biqgemm_exact_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
+        int s = grow(L->d_ws_exact, L->ws_exact_bytes, need);
+        if (s) return s;
+        return bqg_biqgemm_exact_f32(L->d_keys, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu,
+                                     L->d_ws_exact, L->ws_exact_bytes, st);
+    }
+    const size_t need = bqg_biqgemm_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
+    if (need > L->ws_bytes) {
+        int s = grow(L->d_ws, L->ws_bytes, need);
+        if (s) return s;
+        BQG_CUDA(cudaMemsetAsync(L->d_ws, 0, L->ws_bytes, st));
+    }
+    return bqg_biqgemm_f32(L->d_tiled, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu, L->d_ws,
+                           L->ws_bytes, pdl, st);
+}
+
+}  // namespace
+
+extern "C" int bqg_layer_forward_device(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float* d_y,
+                                        int exact, int pdl, void* stream) {
+    if (!L) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null");
+    int s = check_x(x_rows, b, L->n, L->mu, "biqgemm");
+    if (s) return s;
+    std::lock_guard<std::mutex> g(L->mu_lock);
+    return layer_forward(L, d_x, x_rows, b, d_y, exact, pdl, as_stream(stream));
+}
+
+extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_rows, size_t b, float* h_y,
+                                      int exact, bqg_kernel_stats* stats) {
+    if (!L || !h_x || !h_y) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null argument");
+    int s = check_x(x_rows, b, L->n, L->mu, "biqgemm");
+    if (s) return s;
+    std::lock_guard<std::mutex> g(L->mu_lock);
+    s = grow(L->d_x, L->x_cap, sizeof(float) * x_rows * b);
+    if (s) return s;
+    s = grow(L->d_y, L->y_cap, sizeof(float) * L->m * b);
+    if (s) return s;
+    cudaStream_t st = L->stream;
+    if (stats) BQG_CUDA(cudaEventRecord(L->ev[0], st));
+    BQG_CUDA(cudaMemcpyAsync(L->d_x, h_x, sizeof(float) * x_rows * b, cudaMemcpyHostToDevice, st));
+    if (stats) BQG_CUDA(cudaEventRecord(L->ev[1], st));
+    s = layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st);
+    if (s) return s;
+    if (stats) BQG_CUDA(cudaEventRecord(L->ev[2], st));
+    BQG_CUDA(cudaMemcpyAsync(h_y, L->d_y, sizeof(float) * L->m * b, cudaMemcpyDeviceToHost, st));
+    if (stats) BQG_CUDA(cudaEventRecord(L->ev[3], st));
+    BQG_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+        uint64_t ops[4];
+        bqg_op_counters(L->m, L->n, b, L->beta, L->mu, BQG_LUT_DP, ops);
+        stats->lut_build_ops += ops[0];
+        stats->lookups += ops[1];
+        stats->accumulate_ops += ops[2];
+        stats->fma_ops += ops[3];
+        float t01 = 0, t12 = 0, t23 = 0;
+        cudaEventElapsedTime(&t01, L->ev[0], L->ev[1]);
+        cudaEventElapsedTime(&t12, L->ev[1], L->ev[2]);
+        cudaEventElapsedTime(&t23, L->ev[2], L->ev[3]);
+        stats->query_seconds += t12 * 1e-3;
+        stats->replace_seconds += (t01 + t23) * 1e-3;
+    }
+    return BQG_OK;
+}

@@ -1,0 +1,130 @@
+// lut_build.cuh -- in-shared-memory LUT construction (replaces
+// build_lut_block / build_lut_dp, /root/reference/proj/core/include/biqgemm/
+// lut.hpp:50-69,109-154).
+//
+// Placement ("bank-owned"): one CTA owns a block of 32 consecutive groups and
+// BT input columns.  The BT tables of group gb*32+l are interleaved per key
+// and live in the bank(s) lane l owns:
+//     word((k, l, c)) = (k * 32 + l) * BT + c          (k = key, c = column)
+// During the query lane l (which handles group gb*32+l) gathers BT
+// consecutive floats at (k*32+l)*BT: a warp-wide gather touches every bank
+// exactly once per wavefront (LDS.32 / .64 / .128 for BT = 1 / 2 / 4), i.e.
+// it is conflict-free.  Building is conflict-free too: lane l writes a
+// BT-vector into its own slot (STS.32 / .64 / .128).
+//
+// Order of operations (bit-exact with lut.hpp:50-69 evaluated in fp32):
+//   e[0] = ((0 - x0) - x1) - ... - x_{mu-1}
+//   e[k] = e[k - 2^top(k)] + 2*x_top(k)            for 0 < k < 2^(mu-1)
+//   e[2^mu - 1 - k] = -e[k]
+// Unrolled, e[k] = e0 + s_{b1} + s_{b2} + ... over the set bits of k in
+// ascending order, left-associated.  The NW warps of the CTA split the first
+// half into 2^(mu-1-L) chunks of 2^L consecutive keys: warp w runs the DP over
+// the low L bits (identical to the reference's first L rounds), then adds the
+// steps of the chunk index bits in ascending order -- exactly the additions
+// the sequential DP performs for those entries.
+#pragma once
+
+#include "common.cuh"
+
+namespace bqg {
+
+template <int N>
+struct Log2 {
+    static constexpr int value = 1 + Log2<N / 2>::value;
+};
+template <>
+struct Log2<1> {
+    static constexpr int value = 0;
+};
+
+template <int BT>
+struct VecT;
+template <>
+struct VecT<1> {
+    using type = float;
+};
+template <>
+struct VecT<2> {
+    using type = float2;
+};
+template <>
+struct VecT<4> {
+    using type = float4;
+};
+
+template <int BT>
+__device__ __forceinline__ void store_vec(float* dst, const float (&v)[BT], bool negate) {
+    if constexpr (BT == 1) {
+        *dst = negate ? -v[0] : v[0];
+    } else if constexpr (BT == 2) {
+        *reinterpret_cast<float2*>(dst) = negate ? make_float2(-v[0], -v[1]) : make_float2(v[0], v[1]);
+    } else {
+        *reinterpret_cast<float4*>(dst) = negate ? make_float4(-v[0], -v[1], -v[2], -v[3])
+                                                 : make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// Builds, for this lane's group g and input columns col0 .. col0+BT-1, all
+// 2^MU entries into the bank-owned block at `lut` (shared memory).
+//   x : input, x_rows x b row-major (x(r, c) at r*b + c); rows >= x_rows are
+//       zero (lut.hpp:133-136; kernel.hpp:132 lets x be shorter than n).
+//       Columns >= b are clamped to b-1 (their outputs are never stored).
+// Called by all NW warps of the CTA with the same g per lane; warp `warp`
+// writes its chunk.  Caller must __syncthreads() afterwards.
+template <int MU, int NW, int BT>
+__device__ __forceinline__ void build_bank_owned_tables(float* lut, const float* __restrict__ x,
+                                                        long long x_rows, long long b, long long g,
+                                                        long long col0, int warp, int lane) {
+    constexpr int H = 1 << (MU - 1);  // first-half entries
+    constexpr int LOGW = Log2<NW>::value;
+    constexpr int L = (MU - 1) > LOGW ? (MU - 1 - LOGW) : 0;  // low bits per chunk
+    constexpr int NCH = H >> L;                                // chunks (<= NW)
+    constexpr int TABLE = 1 << MU;
+    if (warp >= NCH) return;
+
+    float xv[MU][BT];
+#pragma unroll
+    for (int t = 0; t < MU; ++t) {
+        const long long r = g * MU + t;
+#pragma unroll
+        for (int c = 0; c < BT; ++c) {
+            const long long col = min(col0 + c, b - 1);
+            xv[t][c] = r < x_rows ? ld_cg_f32(x + r * b + col) : 0.0f;
+        }
+    }
+    float low[1 << L][BT];
+#pragma unroll
+    for (int c = 0; c < BT; ++c) {
+        float e0 = 0.0f;
+#pragma unroll
+        for (int t = 0; t < MU; ++t) e0 = __fsub_rn(e0, xv[t][c]);
+        low[0][c] = e0;
+    }
+#pragma unroll
+    for (int i = 1; i <= L; ++i) {
+        const int half = 1 << (i - 1);
+#pragma unroll
+        for (int c = 0; c < BT; ++c) {
+            const float step = 2.0f * xv[i - 1][c];
+#pragma unroll
+            for (int j = 0; j < half; ++j) low[j + half][c] = fadd_rn(low[j][c], step);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < (1 << L); ++j) {
+        float v[BT];
+#pragma unroll
+        for (int c = 0; c < BT; ++c) {
+            v[c] = low[j][c];
+#pragma unroll
+            for (int t = L; t < MU - 1; ++t) {
+                if ((warp >> (t - L)) & 1) v[c] = fadd_rn(v[c], 2.0f * xv[t][c]);
+            }
+        }
+        const int k = (warp << L) + j;
+        store_vec<BT>(lut + (k * 32 + lane) * BT, v, false);
+        store_vec<BT>(lut + ((TABLE - 1 - k) * 32 + lane) * BT, v, true);
+    }
+}
+
+}  // namespace bqg

@@ -1,0 +1,93 @@
+"""Generate the golden fixtures from the REFERENCE itself (oracle/_ref, the
+unmodified reference headers compiled by oracle/Makefile).  Run here, where
+/root/reference exists:
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/cases.npz (small randomized cases mirroring the
+reference's acceptance generators) and tests/golden/configs.npz +
+configs.json (the BASELINE configs' outputs/checksums on the bench_cli data,
+seeds 0x5EED / 0x5EED+1, bench_cli.cpp:106-109).
+"""
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+from oracle.oracle import Reference  # noqa: E402
+
+SEED = 0x5EED
+
+
+def cases(ref):
+    rng = np.random.Generator(np.random.PCG64(1234))
+    out = {}
+    idx = 0
+    for mu in (1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 16):
+        for rep in range(3):
+            m = int(rng.integers(1, 70))
+            n = int(rng.integers(1, 90))
+            b = int(rng.integers(1, 9))
+            beta = int(rng.integers(1, 4))
+            wseed, xseed = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**63))
+            w = ref.random_uniform(m, n, wseed)
+            x = ref.random_normal(n, b, xseed)
+            planes, alpha, keys = ref.quantize_pack(w, beta, mu)
+            y, st = ref.biqgemm(keys, alpha, n, mu, x)
+            yp, _ = ref.biqgemm(keys[:1], None, n, mu, x)
+            G = keys.shape[2]
+            lut_t, ops = ref.build_lut_block(x, 0, G, mu, key_major=False)
+            lut_k, _ = ref.build_lut_block(x, 0, G, mu, key_major=True)
+            p = f"c{idx}_"
+            out[p + "dims"] = np.array([m, n, b, beta, mu, wseed, xseed], np.uint64)
+            out[p + "planes"] = planes
+            out[p + "alpha"] = alpha
+            out[p + "keys"] = keys.astype(np.uint16)
+            out[p + "y"] = y
+            out[p + "yplane"] = yp
+            if mu <= 9:  # keep the fixture small; larger tables are checked live
+                out[p + "lut_t"] = lut_t
+                out[p + "lut_k"] = lut_k
+            out[p + "counters"] = np.array([st["lut_build_ops"], st["lookups"], st["accumulate_ops"]], np.uint64)
+            idx += 1
+    out["count"] = np.array([idx])
+    np.savez_compressed(HERE / "cases.npz", **out)
+    print("cases:", idx)
+
+
+CONFIGS = {
+    "C1": (1024, 1024, 1, 1),
+    "C2": (4096, 4096, 3, 1),
+    "C3": (4096, 4096, 2, 32),
+    "C4b1": (16384, 4096, 3, 1),
+    "C4b8": (16384, 4096, 3, 8),
+}
+
+
+def configs(ref):
+    arrays, meta = {}, {}
+    for name, (m, n, beta, b) in CONFIGS.items():
+        w = ref.random_uniform(m, n, SEED)
+        x = ref.random_normal(n, b, SEED + 1)
+        planes, alpha, keys = ref.quantize_pack(w, beta, 8)
+        y, st = ref.biqgemm(keys, alpha, n, 8, x)
+        meta[name] = dict(m=m, n=n, beta=beta, b=b, mu=8, checksum=float(np.sum(y.astype(np.float64))),
+                          lookups=st["lookups"], lut_build_ops=st["lut_build_ops"],
+                          keys_sha=__import__("hashlib").sha256(keys.astype(np.uint8).tobytes()).hexdigest(),
+                          alpha_sha=__import__("hashlib").sha256(alpha.tobytes()).hexdigest(),
+                          w_sha=__import__("hashlib").sha256(w.tobytes()).hexdigest(),
+                          x_sha=__import__("hashlib").sha256(x.tobytes()).hexdigest())
+        if m * b <= 200_000:
+            arrays[name + "_y"] = y
+        print(name, meta[name]["checksum"])
+    np.savez_compressed(HERE / "configs.npz", **arrays)
+    (HERE / "configs.json").write_text(json.dumps(meta, indent=1))
+
+
+if __name__ == "__main__":
+    r = Reference()
+    cases(r)
+    configs(r)
