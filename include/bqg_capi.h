@@ -139,8 +139,10 @@ int bqg_build_lut_f64(const float* d_x, size_t x_rows, size_t b, unsigned mu, si
  * Fast path (mu <= 8): d_keys is the TILED layout (bqg_tile_keys); fused
  *   LUT build -> query -> alpha epilogue; fp32 LUT, fp32 group sums, fp64
  *   cross-block/plane epilogue.  Deterministic and grid-invariant.
- *   Workspace: bqg_biqgemm_workspace_bytes(); must be zero-filled before the
- *   first call (the kernel leaves it zeroed).  pdl != 0 launches with
+ *   Workspace: bqg_biqgemm_workspace_bytes() bytes (per-block partial sums;
+ *   no initialisation needed).  Two kernels are launched (fused LUT
+ *   build/query, then the fixed-order epilogue), chained with programmatic
+ *   dependent launch.  pdl != 0 also launches the first one with
  *   programmatic stream serialization (overlaps the predecessor's tail).
  * x_rows <= G*mu (rows beyond x_rows are zero; kernel.hpp:132-134). */
 size_t bqg_biqgemm_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu);

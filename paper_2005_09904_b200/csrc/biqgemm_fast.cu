@@ -1,51 +1,71 @@
-// biqgemm_fast.cu -- the fused BiQGEMM hot path for mu <= 8 (fp32 LUT).
+// biqgemm_fast.cu -- the BiQGEMM hot path for mu <= 8 (fp32 LUT), sm_100a.
 //
 // Replaces biqgemm::detail::run + query_rows + the alpha epilogue
 // (/root/reference/proj/core/include/biqgemm/kernel.hpp:83-108,116-204) and
-// build_lut_block (lut.hpp:109-154) with ONE kernel:
+// build_lut_block (lut.hpp:109-154) with two kernels launched back to back
+// with programmatic dependent launch (PDL):
 //
-//   prologue   : each warp issues 128-bit evict-first loads for its first D
-//                work units of packed keys (keys never depend on the previous
-//                kernel, so this runs before griddepcontrol.wait and overlaps
-//                the predecessor's tail under PDL);
-//   LUT build  : after griddepcontrol.wait, the CTA builds the tables of its
-//                32-group block (x BT input columns) in bank-owned shared
-//                memory with the DP recurrence (lut_build.cuh);
-//   query      : per unit (plane i, row tile, group block) lane l gathers
-//                T_{gb*32+l}[key] for 32 (BT=1) or 16 (BT>1) rows from its own
-//                bank -- conflict-free, one wavefront per warp gather -- then a
-//                swizzled butterfly (31 SHFL+FADD per 1024 lookups) sums the
-//                32 groups per row;
-//   epilogue   : the per-(block, plane) partial goes to a workspace; the warp
-//                that completes the last unit of a 32-row tile (atomic ticket)
-//                reduces the tile in a FIXED order -- fp64 over group blocks
-//                ascending, then y = sum_i alpha_i * acc_i in fp64 over planes
-//                ascending (kernel.hpp:183-195) -- and resets the ticket.
+// 1. biqgemm_fast_kernel -- per CTA: one 32-group block x BT input columns x
+//    a contiguous range of 1 KiB key chunks (chunk = plane i x 32-row tile).
+//      producer warp : streams the CTA's key chunks global -> shared with the
+//                      TMA bulk-copy engine (cp.async.bulk, L2 evict-first)
+//                      through an R-stage mbarrier ring.  Keys never depend
+//                      on the previous kernel, so the ring fills before
+//                      griddepcontrol.wait and overlaps the predecessor.
+//      consumer warps: after griddepcontrol.wait, build the block's tables in
+//                      bank-owned shared memory with the DP recurrence
+//                      (lut_build.cuh; table of group g lives in bank g);
+//                      then per chunk lane l owns row l of the tile and at
+//                      step j gathers T_g[key(l, g)] for the rotated group
+//                      g = (l + j) mod 32 -- every lane hits a different bank,
+//                      so each warp gather is one conflict-free wavefront --
+//                      and accumulates in registers.  No cross-lane reduction
+//                      (no SHFL, which shares the shared-memory pipe).  The
+//                      per-(plane, block) partial goes to the workspace.
+// 2. finalize_kernel -- y(r,c) = sum_i alpha_i[r] * sum_gb partial, in fp64,
+//    planes and blocks ascending (kernel.hpp:183-195).
 //
-// The reduction tree of every output is a function of (n, mu) only, so y is
+// Every output's reduction tree is a function of (n, mu) only, so y is
 // bitwise identical for every grid shape, CTA split and row sharding.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
 #include "lut_build.cuh"
+#include "query_core.cuh"
 
 namespace bqg {
 
+// Per-CTA timeline for profiling (BQG_DEBUG_FLAGS & 2): globaltimer ns at
+// start, after the LUT build, after the query, end; smid; clock64 at start/end.
+// Off in production (one predicated branch per CTA).
+__device__ unsigned long long g_timeline[8192][8];
+
 namespace {
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned s;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+    return s;
+}
+
 struct FastPlan {
-    long long upp;    // units per (group block, column tile) pair
-    long long total;  // total units
-    int CT;           // column tiles
-    int H;            // units per (tile, plane): 1 for BT=1 (32 rows), 2 otherwise (16 rows)
-    int mode;         // 0 = aligned (cpb CTAs per pair), 1 = flat contiguous split
-    int cpb;
+    int cpp;    // key chunks (plane x 32-row tile) per (group block, column tile) pair
+    int CT;     // column tiles
+    int mode;   // 0 = aligned (cpb CTAs per pair), 1 = flat contiguous split
+    int cpb;    // aligned: CTAs per pair
     int grid;
+    int q, r;   // balanced split: CTA c gets q + (c < r) chunks of its domain
 };
 
 // Byte offset of key byte `bi` of word w in the bank-owned LUT, OR'd with the
-// lane's column offset.  BT=1: word = k*32 + l  -> byte k<<7 | l<<2.
+// lane's offset.  word(k, l, c) = (k*32 + l)*BT + c  ->  byte = k << SH | l*4*BT.
 template <int MU, int BT>
 __device__ __forceinline__ uint32_t lut_off(uint32_t w, int bi, uint32_t lane_off) {
     constexpr int SH = (BT == 1) ? 7 : (BT == 2 ? 8 : 9);
@@ -55,216 +75,196 @@ __device__ __forceinline__ uint32_t lut_off(uint32_t w, int bi, uint32_t lane_of
     return (v & MASK) | lane_off;
 }
 
-// One unit of keys for this lane: 32 bytes (BT=1) or 16 bytes (BT>1).
-template <int KPU>
-__device__ __forceinline__ void load_keys(uint32_t (&w)[4 * KPU], const uint8_t* a, uint64_t pol) {
-    if constexpr (KPU == 2) {
-        const U8x32 v = ld_stream_u8x32(a);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) w[q] = v.w[q];
-    } else {
-        const uint4 v = ld_stream_u4(a, pol);
-        w[0] = v.x;
-        w[1] = v.y;
-        w[2] = v.z;
-        w[3] = v.w;
-    }
-}
-
-template <int MU, int BT, int NW, int D>
-__global__ void __launch_bounds__(NW * 32, BT == 1 ? 2 : 1)
+template <int MU, int BT, int NW, int R>
+__global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     biqgemm_fast_kernel(const QueryParams p, const FastPlan plan) {
-    extern __shared__ __align__(16) float lut[];
-    constexpr int KPU = (BT == 1) ? 2 : 1;  // uint4 of keys per lane per unit
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    constexpr int LUT_BYTES = (1 << MU) * LutGeom<BT>::KROW * 4;
+    constexpr int SCH = NW;  // chunks per stage (one per consumer warp)
+    constexpr int STAGE_BYTES = SCH * 1024;
+    float* lut = reinterpret_cast<float*>(smem);
+    unsigned char* stages = smem + LUT_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + R * STAGE_BYTES);
+    uint64_t* empty = full + R;
 
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool tl = (p.debug & 2) && threadIdx.x == 0 && blockIdx.x < 8192;
+    if (tl) {
+        g_timeline[blockIdx.x][0] = gtimer();
+        g_timeline[blockIdx.x][5] = smid();
+        g_timeline[blockIdx.x][6] = clock64();
+    }
     pdl_launch_dependents();
 
-    long long ubeg, uend;
-    if (plan.mode == 0) {
-        const long long pair = blockIdx.x / plan.cpb, c = blockIdx.x % plan.cpb;
-        ubeg = pair * plan.upp + plan.upp * c / plan.cpb;
-        uend = pair * plan.upp + plan.upp * (c + 1) / plan.cpb;
-    } else {
-        ubeg = plan.total * blockIdx.x / plan.grid;
-        uend = plan.total * (blockIdx.x + 1) / plan.grid;
+    // This CTA's chunk range [cbeg, cend): 32-bit, no divisions.
+    const int c = plan.mode == 0 ? static_cast<int>(blockIdx.x) % plan.cpb : static_cast<int>(blockIdx.x);
+    const int dom = plan.mode == 0 ? static_cast<int>(blockIdx.x) / plan.cpb : 0;
+    const int cbeg = dom * plan.cpp + c * plan.q + min(c, plan.r);
+    const int cend = cbeg + plan.q + (c < plan.r ? 1 : 0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < R; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int beta = p.beta;
+    const long long rows_pad = static_cast<long long>(p.MT) * 32;
+
+    if (warp == NW) {
+        // ------------------------------------------------ producer (1 lane)
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int sc = 0;  // stage counter across segments
+            for (int seg = cbeg; seg < cend;) {
+                const int pair = seg / plan.cpp;
+                const int pbase = pair * plan.cpp;
+                const int seg_end = min(cend, pbase + plan.cpp);
+                const int gb = pair / plan.CT;
+                const unsigned char* kpair = p.keys + static_cast<long long>(gb) * plan.cpp * 1024;
+                for (int c0 = seg - pbase; c0 < seg_end - pbase; c0 += SCH, ++sc) {
+                    const int cnt = min(SCH, seg_end - pbase - c0);
+                    const int slot = sc % R;
+                    mbar_wait(&empty[slot], ((sc / R) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[slot], cnt * 1024);
+                    bulk_g2s(stages + slot * STAGE_BYTES, kpair + static_cast<long long>(c0) * 1024, cnt * 1024,
+                             &full[slot], pol);
+                }
+                seg = seg_end;
+            }
+        }
+        return;
     }
 
-    const int beta = p.beta, H = plan.H;
-    const long long MT = p.MT, rows_pad = MT * 32;
-    const uint32_t lane_off = static_cast<uint32_t>(lane) * 4u * BT;
-    const char* lutc = reinterpret_cast<const char*>(lut);
-    const uint64_t pol = policy_evict_first();
-    bool waited = false;
+    // ---------------------------------------------------- consumers
+    uint32_t goff[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) goff[j] = static_cast<uint32_t>((lane + j) & 31) * 4u * BT;
+    const uint32_t lut_s = smem_u32(lut);
+    pdl_wait();  // x (and the workspace) of the predecessor are visible from here on
+    if (tl) g_timeline[blockIdx.x][1] = gtimer();
+    int sc = 0;
+    for (int seg = cbeg; seg < cend;) {
+        const int pair = seg / plan.cpp;
+        const int pbase = pair * plan.cpp;
+        const int seg_end = min(cend, pbase + plan.cpp);
+        const int gb = pair / plan.CT, ct = pair - gb * plan.CT;
+        if (seg != cbeg) named_bar_sync(1, NW * 32);  // previous segment done with the LUT
+        build_bank_owned_tables<MU, NW, BT, LutGeom<BT>::KROW>(lut, p.x, p.x_rows, p.b,
+                                                               static_cast<long long>(gb) * 32 + lane,
+                                                               static_cast<long long>(ct) * BT, warp, lane);
+        named_bar_sync(1, NW * 32);
+        if (tl) g_timeline[blockIdx.x][2] = gtimer();
 
-    for (long long seg = ubeg; seg < uend;) {
-        const long long pair = seg / plan.upp;
-        const long long seg_end = min(uend, (pair + 1) * plan.upp);
-        const int gb = static_cast<int>(pair / plan.CT), ct = static_cast<int>(pair % plan.CT);
-        const long long base_local = pair * plan.upp;
-
-        // Address of this lane's keys for unit u (global index).
-        auto key_addr = [&](long long u) -> const uint8_t* {
-            const long long local = u - base_local;
-            const long long t = local / (static_cast<long long>(beta) * H);
-            const int rem = static_cast<int>(local - t * beta * H);
-            const int i = rem / H, h = rem - (rem / H) * H;
-            const uint8_t* chunk =
-                p.keys + ((((static_cast<long long>(gb) * beta + i) * MT + t) * 32 + lane) * 32);
-            if (BT == 1) return chunk;
-            return chunk + 16 * (h ^ (lane >> 4));
-        };
-
-        uint32_t kr[D][4 * KPU];
+        const int lo = seg - pbase, hi = seg_end - pbase;
+        // (t, i) of this warp's chunk lo + warp, advanced by NW = q*beta + rr per stage
+        int ti = (lo + warp) / beta;
+        int ii = lo + warp - ti * beta;
+        const int dq = NW / beta, dr = NW - (NW / beta) * beta;
+        for (int c0 = lo; c0 < hi; c0 += SCH, ++sc) {
+            const int slot = sc % R;
+            mbar_wait(&full[slot], (sc / R) & 1);
+            if (tl && sc == 0) g_timeline[blockIdx.x][3] = gtimer();
+            const int chunk = c0 + warp;
+            if (chunk < hi) {
+                const unsigned char* kc = stages + slot * STAGE_BYTES + warp * 1024;
+                const uint4 ka = *reinterpret_cast<const uint4*>(kc + lane * 16);
+                const uint4 kb = *reinterpret_cast<const uint4*>(kc + 512 + lane * 16);
+                const uint32_t w[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+                float o[BT];
+                gather_chunk<MU, BT>(w, lut_s, goff, o);
+                float* dst = p.partial + ((static_cast<long long>(ii) * p.NB + gb) * rows_pad + ti * 32 + lane) * p.b +
+                             static_cast<long long>(ct) * BT;
 #pragma unroll
-        for (int s = 0; s < D; ++s) {
-            const long long u = seg + warp + static_cast<long long>(s) * NW;
-            if (u < seg_end) load_keys<KPU>(kr[s], key_addr(u), pol);
-        }
-        if (!waited) {
-            pdl_wait();
-            waited = true;
-        }
-        __syncthreads();  // previous segment's gathers are done with the LUT
-        build_bank_owned_tables<MU, NW, BT>(lut, p.x, p.x_rows, p.b,
-                                            static_cast<long long>(gb) * 32 + lane,
-                                            static_cast<long long>(ct) * BT, warp, lane);
-        __syncthreads();
-
-        for (long long ub = seg + warp; ub < seg_end; ub += static_cast<long long>(D) * NW) {
-#pragma unroll
-            for (int s = 0; s < D; ++s) {
-                const long long u = ub + static_cast<long long>(s) * NW;
-                if (u >= seg_end) break;
-                uint32_t w[4 * KPU];
-#pragma unroll
-                for (int q = 0; q < 4 * KPU; ++q) w[q] = kr[s][q];
-                {
-                    const long long un = u + static_cast<long long>(D) * NW;
-                    if (un < seg_end) load_keys<KPU>(kr[s], key_addr(un), pol);
-                }
-                const long long local = u - base_local;
-                const long long t = local / (static_cast<long long>(beta) * H);
-                const int rem = static_cast<int>(local - t * beta * H);
-                const int i = rem / H, h = rem - (rem / H) * H;
-
-                if constexpr (BT == 1) {
-                    float v[32];
-#pragma unroll
-                    for (int wi = 0; wi < 8; ++wi) {
-#pragma unroll
-                        for (int bi = 0; bi < 4; ++bi) {
-                            const uint32_t off = lut_off<MU, 1>(w[wi], bi, lane_off);
-                            v[wi * 4 + bi] = *reinterpret_cast<const float*>(lutc + off);
-                        }
-                    }
-                    // swizzled butterfly: slot s holds row s ^ lane
-#pragma unroll
-                    for (int hw = 16; hw >= 1; hw >>= 1) {
-#pragma unroll
-                        for (int s2 = 0; s2 < hw; ++s2)
-                            v[s2] += __shfl_xor_sync(0xffffffffu, v[s2 + hw], hw);
-                    }
-                    const long long r = t * 32 + lane;
-                    p.partial[(static_cast<long long>(gb) * beta + i) * rows_pad + r] = v[0];
-                } else {
-                    float v[16][BT];
-#pragma unroll
-                    for (int wi = 0; wi < 4; ++wi) {
-#pragma unroll
-                        for (int bi = 0; bi < 4; ++bi) {
-                            const uint32_t off = lut_off<MU, BT>(w[wi], bi, lane_off);
-                            if constexpr (BT == 2) {
-                                const float2 e = *reinterpret_cast<const float2*>(lutc + off);
-                                v[wi * 4 + bi][0] = e.x;
-                                v[wi * 4 + bi][1] = e.y;
-                            } else {
-                                const float4 e = *reinterpret_cast<const float4*>(lutc + off);
-                                v[wi * 4 + bi][0] = e.x;
-                                v[wi * 4 + bi][1] = e.y;
-                                v[wi * 4 + bi][2] = e.z;
-                                v[wi * 4 + bi][3] = e.w;
-                            }
-                        }
-                    }
-                    // slot s holds row 16h + (s ^ (lane & 15))
-#pragma unroll
-                    for (int hw = 8; hw >= 1; hw >>= 1) {
-#pragma unroll
-                        for (int s2 = 0; s2 < hw; ++s2) {
-#pragma unroll
-                            for (int c = 0; c < BT; ++c)
-                                v[s2][c] += __shfl_xor_sync(0xffffffffu, v[s2 + hw][c], hw);
-                        }
-                    }
-#pragma unroll
-                    for (int c = 0; c < BT; ++c) v[0][c] += __shfl_xor_sync(0xffffffffu, v[0][c], 16);
-                    if (lane < 16) {
-                        const long long r = t * 32 + 16 * h + lane;
-                        float* dst = p.partial +
-                                     ((static_cast<long long>(gb) * beta + i) * rows_pad + r) * p.b +
-                                     static_cast<long long>(ct) * BT;
-#pragma unroll
-                        for (int c = 0; c < BT; ++c) {
-                            if (ct * BT + c < p.b) dst[c] = v[0][c];
-                        }
-                    }
-                }
-
-                // ---- completion ticket for (tile t, column tile ct) ----
-                __threadfence();
-                __syncwarp();
-                unsigned ticket = 0;
-                unsigned* ctr = p.counters + t * plan.CT + ct;
-                if (lane == 0) ticket = atomicAdd(ctr, 1u);
-                ticket = __shfl_sync(0xffffffffu, ticket, 0);
-                const unsigned expect = static_cast<unsigned>(p.NB) * beta * H;
-                if (ticket == expect - 1) {
-                    __threadfence();
-                    const long long r = t * 32 + lane;
-                    if (r < p.m) {
-                        for (int c = 0; c < BT; ++c) {
-                            const long long col = static_cast<long long>(ct) * BT + c;
-                            if (col >= p.b) break;
-                            double y = 0.0;
-                            for (int pi = 0; pi < beta; ++pi) {
-                                double acc = 0.0;
-                                for (int g2 = 0; g2 < p.NB; ++g2) {
-                                    acc += static_cast<double>(ld_cg_f32(
-                                        p.partial +
-                                        ((static_cast<long long>(g2) * beta + pi) * rows_pad + r) * p.b +
-                                        col));
-                                }
-                                const double a =
-                                    p.alpha ? static_cast<double>(p.alpha[static_cast<long long>(pi) * p.m + r])
-                                            : 1.0;
-                                y += a * acc;
-                            }
-                            p.y[r * p.b + col] = static_cast<float>(y);
-                        }
-                    }
-                    if (lane == 0) *ctr = 0u;
-                }
+                for (int cc = 0; cc < BT; ++cc)
+                    if (ct * BT + cc < p.b) dst[cc] = o[cc];
             }
+            ti += dq;
+            ii += dr;
+            if (ii >= beta) {
+                ii -= beta;
+                ++ti;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
         }
         seg = seg_end;
     }
-    if (!waited) pdl_wait();
+    if (tl) {
+        g_timeline[blockIdx.x][4] = gtimer();
+        g_timeline[blockIdx.x][7] = clock64();
+    }
+}
+
+// y(r, c) = sum_i alpha_i[r] * (sum_gb partial[i][gb][r][c]), fp64, ascending
+// planes and group blocks (kernel.hpp:183-195).  One thread per output;
+// loads issued 16 at a time.
+__global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long long>(p.m) * p.b) return;
+    const long long r = idx / p.b;
+    const long long rows_pad = static_cast<long long>(p.MT) * 32;
+    const int total = p.NB * p.beta;  // q = i*NB + gb
+    const long long stride = rows_pad * p.b;
+    const float* src = p.partial + idx;  // row r, column c of partial q = 0
+    double y = 0.0, acc = 0.0;
+    int g = 0, i = 0;
+    double a_i = p.alpha ? static_cast<double>(__ldg(p.alpha + r)) : 1.0;
+#pragma unroll 1
+    for (int q0 = 0; q0 < total; q0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = __ldcg(src + min(q0 + k, total - 1) * stride);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (q0 + k < total) {
+                acc += static_cast<double>(v[k]);
+                if (++g == p.NB) {
+                    y += a_i * acc;
+                    acc = 0.0;
+                    g = 0;
+                    ++i;
+                    if (i < p.beta && p.alpha)
+                        a_i = static_cast<double>(__ldg(p.alpha + static_cast<long long>(i) * p.m + r));
+                }
+            }
+        }
+    }
+    p.y[idx] = static_cast<float>(y);
+}
+
+constexpr int kNW = 8;
+
+template <int BT>
+constexpr int stages_for() {
+    return BT == 1 ? 6 : (BT == 2 ? 4 : 6);
+}
+
+template <int MU, int BT>
+size_t smem_bytes() {
+    return static_cast<size_t>(1u << MU) * LutGeom<BT>::KROW * 4 + static_cast<size_t>(stages_for<BT>()) * kNW * 1024 +
+           2 * stages_for<BT>() * sizeof(uint64_t);
 }
 
 template <int MU, int BT>
 cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, cudaStream_t stream) {
-    constexpr int NW = 8, D = 4;
-    auto kern = biqgemm_fast_kernel<MU, BT, NW, D>;
-    const size_t smem = static_cast<size_t>(1u << MU) * 32 * BT * sizeof(float);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
+    constexpr int R = stages_for<BT>();
+    auto kern = biqgemm_fast_kernel<MU, BT, kNW, R>;
+    const size_t smem = smem_bytes<MU, BT>();
+    static bool configured = false;  // one attribute call per instantiation
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
+        configured = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(plan.grid));
-    cfg.blockDim = dim3(NW * 32);
+    cfg.blockDim = dim3((kNW + 1) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -272,7 +272,20 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, p, plan);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, plan);
+    if (e != cudaSuccess) return e;
+    // finaliser: always PDL-chained to the fused kernel
+    cudaLaunchConfig_t f = {};
+    const long long n = static_cast<long long>(p.m) * p.b;
+    f.gridDim = dim3(static_cast<unsigned>((n + 127) / 128));
+    f.blockDim = dim3(128);
+    f.stream = stream;
+    cudaLaunchAttribute fa[1];
+    fa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    fa[0].val.programmaticStreamSerializationAllowed = 1;
+    f.attrs = fa;
+    f.numAttrs = 1;
+    return cudaLaunchKernelEx(&f, finalize_kernel, p);
 }
 
 template <int MU>
@@ -289,42 +302,43 @@ FastPlan make_plan(long long m, long long groups, int beta, long long b, int mu,
     FastPlan pl{};
     const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
     pl.CT = static_cast<int>((b + BT - 1) / BT);
-    pl.H = BT == 1 ? 1 : 2;
-    pl.upp = MT * beta * pl.H;
+    pl.cpp = static_cast<int>(MT * beta);
     const long long pairs = NB * pl.CT;
-    pl.total = pairs * pl.upp;
-    // Cost model in shared-memory wavefronts (the binding resource):
-    // building one block of tables = 2^mu * BT wavefronts; one unit =
-    // 32 (BT<=2) or 64 (BT=4) gather wavefronts.
-    const double build = static_cast<double>(1 << mu) * BT + 64.0;
-    const double unit = BT == 4 ? 64.0 : 32.0;
+    const long long total = pairs * pl.cpp;
+    // Cost model in shared-memory wavefronts (the binding resource): building
+    // one block of tables = 2^mu * BT wavefronts (+ fixed overhead); one
+    // chunk = 32 (BT=1), 64 (BT=2) or 128 (BT=4) gather wavefronts + 8 key
+    // wavefronts.
+    const double build = static_cast<double>(1 << mu) * BT + 96.0;
+    const double unit = (BT == 4 ? 128.0 : (BT == 2 ? 64.0 : 32.0)) + 8.0;  // gather + key wavefronts
     const long long sms = std::max(1, num_sms);
-    // aligned: cpb CTAs per pair
     long long best_cpb = 1;
     double best_aligned = 1e300;
-    for (long long cpb = 1; cpb <= std::max<long long>(1, std::min<long long>(pl.upp, 4 * sms)); ++cpb) {
+    for (long long cpb = 1; cpb <= std::max<long long>(1, std::min<long long>(pl.cpp, 4 * sms)); ++cpb) {
         const long long grid = pairs * cpb;
         const long long waves = (grid + sms - 1) / sms;
-        const double t = static_cast<double>(waves) *
-                         (build + static_cast<double>((pl.upp + cpb - 1) / cpb) * unit);
+        const double t = static_cast<double>(waves) * (build + static_cast<double>((pl.cpp + cpb - 1) / cpb) * unit);
         if (t < best_aligned - 1e-9) {
             best_aligned = t;
             best_cpb = cpb;
         }
     }
-    // flat: one CTA per SM, contiguous chunks (may span several pairs)
-    const long long fgrid = std::min<long long>(sms, pl.total);
-    const long long chunk = (pl.total + fgrid - 1) / fgrid;
-    const long long spans = std::min<long long>(pairs, (chunk + pl.upp - 1) / pl.upp + 1);
+    const long long fgrid = std::min<long long>(sms, total);
+    const long long chunk = (total + fgrid - 1) / fgrid;
+    const long long spans = std::min<long long>(pairs, (chunk + pl.cpp - 1) / pl.cpp + 1);
     const double t_flat = static_cast<double>(spans) * build + static_cast<double>(chunk) * unit;
     if (t_flat < best_aligned) {
         pl.mode = 1;
         pl.cpb = 1;
         pl.grid = static_cast<int>(fgrid);
+        pl.q = static_cast<int>(total / fgrid);
+        pl.r = static_cast<int>(total % fgrid);
     } else {
         pl.mode = 0;
         pl.cpb = static_cast<int>(best_cpb);
         pl.grid = static_cast<int>(pairs * best_cpb);
+        pl.q = pl.cpp / pl.cpb;
+        pl.r = pl.cpp % pl.cpb;
     }
     return pl;
 }
@@ -333,21 +347,31 @@ FastPlan make_plan(long long m, long long groups, int beta, long long b, int mu,
 
 size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b) {
     const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
-    const int BT = pick_bt(b);
-    const long long CT = (b + BT - 1) / BT;
-    const size_t partial = static_cast<size_t>(NB) * beta * MT * 32 * b * sizeof(float);
-    const size_t counters = static_cast<size_t>(MT * CT) * sizeof(unsigned);
-    return ((counters + 255) / 256) * 256 + partial;
+    return static_cast<size_t>(NB) * beta * MT * 32 * b * sizeof(float);
 }
 
 int plan_cpb(long long m, long long groups, int beta, long long b, int num_sms) {
     return make_plan(m, groups, beta, b, 8, num_sms).cpb;
 }
 
-cudaError_t launch_biqgemm_fast(const QueryParams& p, int mu, bool pdl, cudaStream_t stream) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaStream_t stream) {
+    static const int debug_flags = [] {
+        const char* e = getenv("BQG_DEBUG_FLAGS");  // profiling switches; never set in production
+        return e ? atoi(e) : 0;
+    }();
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    QueryParams p = p_in;
+    p.debug = debug_flags;
+    if (!(debug_flags & 128)) {  // 128: force the two-kernel form (profiling)
+        bool used = false;
+        cudaError_t e = launch_biqgemm_cluster(p, mu, pdl, stream, &used);
+        if (e != cudaSuccess || used) return e;
+    }
     const FastPlan plan = make_plan(p.m, p.G, p.beta, p.b, mu, sms);
     const int bt = pick_bt(p.b);
     switch (mu) {
@@ -383,8 +407,7 @@ __global__ void __launch_bounds__(256) build_lut_dump_kernel(const float* __rest
         const long long g = static_cast<long long>(blockIdx.x) * 32 + l;
         if (g >= count) continue;
         const long long base = g * b * TABLE;
-        const long long o = key_major ? base + static_cast<long long>(k) * b + col
-                                      : base + col * TABLE + k;
+        const long long o = key_major ? base + static_cast<long long>(k) * b + col : base + col * TABLE + k;
         out[o] = tab[idx];
     }
 }
@@ -415,3 +438,10 @@ cudaError_t launch_build_lut_f32(const float* x, long long x_rows, long long b, 
 }
 
 }  // namespace bqg
+
+extern "C" int bqg_debug_timeline(unsigned long long* out, int rows) {
+    return cudaMemcpyFromSymbol(out, bqg::g_timeline, sizeof(unsigned long long) * 8 * (rows < 8192 ? rows : 8192)) ==
+                   cudaSuccess
+               ? 0
+               : 2;
+}

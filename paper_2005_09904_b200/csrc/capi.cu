@@ -411,22 +411,16 @@ bqg::QueryParams make_params(const uint8_t* keys, const float* alpha, const floa
                              size_t m, size_t n, size_t b, unsigned beta, unsigned mu, void* ws) {
     bqg::QueryParams p{};
     const long long G = static_cast<long long>(groups_of(n, mu));
-    const long long MT = (static_cast<long long>(m) + 31) / 32;
-    const long long NB = (G + 31) / 32;
-    const int BT = b == 1 ? 1 : (b == 2 ? 2 : 4);
-    const long long CT = (static_cast<long long>(b) + BT - 1) / BT;
-    const size_t ctr_bytes = ((static_cast<size_t>(MT * CT) * sizeof(unsigned) + 255) / 256) * 256;
     p.keys = keys;
     p.alpha = alpha;
     p.x = x;
     p.y = y;
-    p.counters = static_cast<unsigned*>(ws);
-    p.partial = reinterpret_cast<float*>(static_cast<char*>(ws) + ctr_bytes);
+    p.partial = static_cast<float*>(ws);
     p.x_rows = static_cast<long long>(x_rows);
     p.m = static_cast<int>(m);
     p.G = static_cast<int>(G);
-    p.NB = static_cast<int>(NB);
-    p.MT = static_cast<int>(MT);
+    p.NB = static_cast<int>((G + 31) / 32);
+    p.MT = static_cast<int>((static_cast<long long>(m) + 31) / 32);
     p.beta = static_cast<int>(beta);
     p.b = static_cast<int>(b);
     p.cpb = 1;
@@ -446,6 +440,11 @@ extern "C" int bqg_biqgemm_f32(const uint8_t* d_keys, const float* d_alpha, cons
     s = check_x(x_rows, b, n, mu, "biqgemm");
     if (s) return s;
     if (m > 0x7fffffff || b > 0x7fffffff) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: dimension too large");
+    {
+        const unsigned long long chunks = ((groups_of(n, mu) + 31) / 32) * ((m + 31) / 32) * beta *
+                                          ((b + 3) / 4 + 1);
+        if (chunks > 0x7fffffffull) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: problem too large for one call");
+    }
     if (!d_keys || !d_x || !d_y || !d_ws) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null pointer");
     if (ws_bytes < bqg_biqgemm_workspace_bytes(m, n, b, beta, mu))
         return set_err(BQG_ERR_WORKSPACE, "biqgemm: workspace %zu < %zu bytes", ws_bytes,
@@ -746,7 +745,6 @@ int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float
     if (need > L->ws_bytes) {
         int s = grow(L->d_ws, L->ws_bytes, need);
         if (s) return s;
-        BQG_CUDA(cudaMemsetAsync(L->d_ws, 0, L->ws_bytes, st));
     }
     return bqg_biqgemm_f32(L->d_tiled, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu, L->d_ws,
                            L->ws_bytes, pdl, st);

@@ -56,11 +56,13 @@ __device__ __forceinline__ uint4 ld_stream_u4(const void* p, uint64_t pol) {
     return v;
 }
 
-__device__ __forceinline__ float ld_cg_f32(const float* p) {
-    float v;
-    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
+// L2-coherent load (bypasses L1) that the compiler may schedule freely.
+__device__ __forceinline__ float ld_cg_f32(const float* p) { return __ldcg(p); }
+
+// Release/acquire fence at GPU scope (lighter than __threadfence's SC fence):
+// orders this thread's partial stores before its ticket atomic, and the
+// finaliser's ticket observation before its partial loads.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // ---- shared memory --------------------------------------------------------------
 
@@ -95,5 +97,81 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 // Exact IEEE fp32 add that ptxas may not contract or reorder: the LUT entries
 // must follow the DP recurrence of lut.hpp:50-69 operation for operation.
 __device__ __forceinline__ float fadd_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// ---- mbarrier + bulk copy (TMA engine, non-tensor) ---------------------------
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}"
+        ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+// Global -> shared bulk copy completed on `bar` (complete_tx), L2 policy hint.
+// bytes % 16 == 0, both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+// Named barrier over `count` threads (the consumer warps only).
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// ---- thread-block clusters ---------------------------------------------------
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// Distributed shared memory: the address of the same shared-memory offset in
+// CTA `rank` of this cluster, and a load through it.
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t caddr) {
+    float v;
+    asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(caddr));
+    return v;
+}
+
+// Cluster-wide barrier with release/acquire semantics: global-memory writes of
+// every CTA in the cluster before the arrive are visible to every CTA after
+// the wait.  All threads of every CTA must execute it.
+__device__ __forceinline__ void cluster_sync_acqrel() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Cluster barrier without memory ordering (e.g. "nobody exits while others
+// still read my shared memory").
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 
 }  // namespace bqg

@@ -8,12 +8,15 @@
 //   keys     beta x m x G, u8 for mu <= 8, u16 for mu > 8, pad bits 0
 //            (KeyMatrix, packing.hpp:61-73; the BQGM on-disk key payload,
 //            model_io.cpp:77-87)
-//   tiled    (mu <= 8) NB x beta x MT x 32 x 32 bytes, NB = ceil(G/32),
-//            MT = ceil(m/32): for group block gb, plane i, row tile t the
-//            1 KiB chunk holds, for lane gl (group gb*32+gl), the 32 keys of
-//            rows t*32 .. t*32+31 at byte position rr ^ gl.  A warp streams
-//            one contiguous 1 KiB chunk per (plane, row tile); the XOR
-//            swizzle lets the cross-lane reduction run without selects.
+//   tiled    (mu <= 8) 1 KiB chunks, chunk(gb, t, i) at ((gb*MT + t)*beta + i)
+//            KiB, NB = ceil(G/32), MT = ceil(m/32): group block gb, row tile
+//            t, plane i.  Inside a chunk, lane l (row t*32 + l) owns the
+//            16-byte pieces at l*16 and 512 + l*16; its byte j (piece j>>4,
+//            byte j&15) is the key of group gb*32 + ((l + j) mod 32).  A CTA's
+//            chunk range is one contiguous byte range (one TMA bulk copy per
+//            pipeline stage); a warp's 16-byte shared-memory reads are
+//            conflict-free; the rotation makes lane l read bank (l+j) mod 32
+//            at step j, so the LUT gather never conflicts.
 //   x        x_rows x b f32 (x_rows <= G*mu; missing rows are zero)
 //   y        m x b f32
 #pragma once
@@ -28,10 +31,10 @@ struct QueryParams {
     const float* alpha;     // beta x m or nullptr (plane mode: alpha = 1)
     const float* x;         // x_rows x b
     float* y;               // m x b
-    float* partial;         // NB x beta x (MT*32) x b   (workspace)
-    unsigned* counters;     // MT                        (workspace, zero, left zero)
+    float* partial;         // beta x NB x (MT*32) x b   (workspace, plane-major)
     long long x_rows;
     int m, G, NB, MT, beta, b, cpb;
+    int debug;  // profiling switches (BQG_DEBUG_FLAGS); 0 in production
 };
 
 // Workspace for the fast path (bytes).
@@ -48,7 +51,11 @@ cudaError_t launch_tile_keys(const uint8_t* keys, long long m, long long groups,
                              uint8_t* tiled, cudaStream_t stream);
 
 // Fast path (mu <= 8): fused LUT build -> query -> alpha epilogue.
+// Tries the single-kernel cluster form first, else two PDL-chained kernels.
 cudaError_t launch_biqgemm_fast(const QueryParams& p, int mu, bool pdl, cudaStream_t stream);
+// Single-kernel form with an in-cluster reduction; *used = false when the
+// device cannot co-schedule the cluster (caller falls back).
+cudaError_t launch_biqgemm_cluster(const QueryParams& p, int mu, bool pdl, cudaStream_t stream, bool* used);
 
 // Fast-path LUT builder exposed for parity (same device code as the fused kernel).
 cudaError_t launch_build_lut_f32(const float* x, long long x_rows, long long b, int mu,

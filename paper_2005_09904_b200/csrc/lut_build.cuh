@@ -5,7 +5,8 @@
 // Placement ("bank-owned"): one CTA owns a block of 32 consecutive groups and
 // BT input columns.  The BT tables of group gb*32+l are interleaved per key
 // and live in the bank(s) lane l owns:
-//     word((k, l, c)) = (k * 32 + l) * BT + c          (k = key, c = column)
+//     word((k, l, c)) = k * KROW + l * BT + c          (k = key, c = column)
+// with KROW = 32*BT (or 64 for BT = 1, see the query kernel).
 // During the query lane l (which handles group gb*32+l) gathers BT
 // consecutive floats at (k*32+l)*BT: a warp-wide gather touches every bank
 // exactly once per wavefront (LDS.32 / .64 / .128 for BT = 1 / 2 / 4), i.e.
@@ -71,27 +72,50 @@ __device__ __forceinline__ void store_vec(float* dst, const float (&v)[BT], bool
 //       Columns >= b are clamped to b-1 (their outputs are never stored).
 // Called by all NW warps of the CTA with the same g per lane; warp `warp`
 // writes its chunk.  Caller must __syncthreads() afterwards.
-template <int MU, int NW, int BT>
+// KROW: words per key row (>= 32*BT).  The query kernel uses KROW = 64 for
+// BT = 1 so that a key sits at bit 8 of the byte address (PRMT addressing).
+template <int MU, int NW, int BT, int KROW = 32 * BT>
 __device__ __forceinline__ void build_bank_owned_tables(float* lut, const float* __restrict__ x,
                                                         long long x_rows, long long b, long long g,
                                                         long long col0, int warp, int lane) {
-    constexpr int H = 1 << (MU - 1);  // first-half entries
-    constexpr int LOGW = Log2<NW>::value;
-    constexpr int L = (MU - 1) > LOGW ? (MU - 1 - LOGW) : 0;  // low bits per chunk
-    constexpr int NCH = H >> L;                                // chunks (<= NW)
+    constexpr int L = (MU - 1) < 2 ? (MU - 1) : 2;  // low bits per chunk (chunk = 2^L keys)
+    constexpr int NCH = 1 << (MU - 1 - L);           // chunks in the first half
     constexpr int TABLE = 1 << MU;
     if (warp >= NCH) return;
 
     float xv[MU][BT];
+    if constexpr (BT == 1 && MU % 4 == 0) {
+        // b == 1 here (BT = 1 is only used for one input column): the group's
+        // MU inputs are contiguous -> 16-byte loads.
+        const long long r0 = g * MU;
+        if (b == 1 && r0 + MU <= x_rows && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
 #pragma unroll
-    for (int t = 0; t < MU; ++t) {
-        const long long r = g * MU + t;
+            for (int q = 0; q < MU / 4; ++q) {
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(x + r0 + 4 * q));
+                xv[4 * q + 0][0] = v.x;
+                xv[4 * q + 1][0] = v.y;
+                xv[4 * q + 2][0] = v.z;
+                xv[4 * q + 3][0] = v.w;
+            }
+        } else {
 #pragma unroll
-        for (int c = 0; c < BT; ++c) {
-            const long long col = min(col0 + c, b - 1);
-            xv[t][c] = r < x_rows ? ld_cg_f32(x + r * b + col) : 0.0f;
+            for (int t = 0; t < MU; ++t) {
+                const long long r = r0 + t;
+                xv[t][0] = r < x_rows ? ld_cg_f32(x + r * b + min(col0, b - 1)) : 0.0f;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < MU; ++t) {
+            const long long r = g * MU + t;
+#pragma unroll
+            for (int c = 0; c < BT; ++c) {
+                const long long col = min(col0 + c, b - 1);
+                xv[t][c] = r < x_rows ? ld_cg_f32(x + r * b + col) : 0.0f;
+            }
         }
     }
+    // e0 and the low-chunk DP (identical to the reference's first L rounds)
     float low[1 << L][BT];
 #pragma unroll
     for (int c = 0; c < BT; ++c) {
@@ -99,31 +123,33 @@ __device__ __forceinline__ void build_bank_owned_tables(float* lut, const float*
 #pragma unroll
         for (int t = 0; t < MU; ++t) e0 = __fsub_rn(e0, xv[t][c]);
         low[0][c] = e0;
-    }
 #pragma unroll
-    for (int i = 1; i <= L; ++i) {
-        const int half = 1 << (i - 1);
-#pragma unroll
-        for (int c = 0; c < BT; ++c) {
+        for (int i = 1; i <= L; ++i) {
             const float step = 2.0f * xv[i - 1][c];
+            const int half = 1 << (i - 1);
 #pragma unroll
             for (int j = 0; j < half; ++j) low[j + half][c] = fadd_rn(low[j][c], step);
         }
     }
+#pragma unroll 1
+    for (int ch = warp; ch < NCH; ch += NW) {
 #pragma unroll
-    for (int j = 0; j < (1 << L); ++j) {
-        float v[BT];
+        for (int j = 0; j < (1 << L); ++j) {
+            float v[BT];
 #pragma unroll
-        for (int c = 0; c < BT; ++c) {
-            v[c] = low[j][c];
+            for (int c = 0; c < BT; ++c) {
+                float e = low[j][c];
 #pragma unroll
-            for (int t = L; t < MU - 1; ++t) {
-                if ((warp >> (t - L)) & 1) v[c] = fadd_rn(v[c], 2.0f * xv[t][c]);
+                for (int t = L; t < MU - 1; ++t) {
+                    const float st = 2.0f * xv[t][c];
+                    e = ((ch >> (t - L)) & 1) ? fadd_rn(e, st) : e;
+                }
+                v[c] = e;
             }
+            const int k = (ch << L) + j;
+            store_vec<BT>(lut + k * KROW + lane * BT, v, false);
+            store_vec<BT>(lut + (TABLE - 1 - k) * KROW + lane * BT, v, true);
         }
-        const int k = (warp << L) + j;
-        store_vec<BT>(lut + (k * 32 + lane) * BT, v, false);
-        store_vec<BT>(lut + ((TABLE - 1 - k) * 32 + lane) * BT, v, true);
     }
 }
 

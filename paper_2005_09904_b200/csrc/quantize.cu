@@ -108,23 +108,26 @@ __global__ void pack_keys_kernel(const uint32_t* __restrict__ plane, long long m
 }
 
 // Row-major u8 keys [beta][m][G] -> tiled layout (see kernels.h):
-//   byte((i, r, g)) = ((((gb*beta + i)*MT + t)*32 + gl)*32 + (rr ^ gl))
-// with gb = g/32, gl = g%32, t = r/32, rr = r%32.  Padding rows/groups are 0.
-// One thread per output byte (coalesced writes).
+//   chunk(gb, t, i) = ((gb*MT + t)*beta + i) * 1024 bytes
+//   within a chunk, lane l (row t*32 + l) owns the 16-byte pieces at l*16 and
+//   512 + l*16; its byte j (piece j>>4, byte j&15) is the key of group
+//   gb*32 + ((l + j) mod 32).
+// Padding rows/groups are 0.  One thread per output byte (coalesced writes).
 __global__ void tile_keys_kernel(const uint8_t* __restrict__ keys, long long m, long long groups,
                                  int beta, long long MT, long long NB, uint8_t* __restrict__ out) {
-    const long long total = NB * beta * MT * 1024;
+    const long long total = NB * MT * beta * 1024;
     const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= total) return;
-    const int pos = static_cast<int>(idx & 31);
-    const int gl = static_cast<int>((idx >> 5) & 31);
-    long long rest = idx >> 10;
-    const long long t = rest % MT;
-    rest /= MT;
-    const int i = static_cast<int>(rest % beta);
-    const long long gb = rest / beta;
-    const int rr = pos ^ gl;
-    const long long r = t * 32 + rr, g = gb * 32 + gl;
+    const int within = static_cast<int>(idx & 1023);
+    const int l = (within >> 4) & 31;
+    const int j = ((within >> 9) << 4) | (within & 15);
+    const int gl = (l + j) & 31;
+    long long chunk = idx >> 10;
+    const int i = static_cast<int>(chunk % beta);
+    chunk /= beta;
+    const long long t = chunk % MT;
+    const long long gb = chunk / MT;
+    const long long r = t * 32 + l, g = gb * 32 + gl;
     uint8_t v = 0;
     if (r < m && g < groups) v = keys[(static_cast<long long>(i) * m + r) * groups + g];
     out[idx] = v;

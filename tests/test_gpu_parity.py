@@ -39,12 +39,14 @@ def tile_numpy(keys, mu):
     """The tiled layout of kernels.h restated in numpy."""
     beta, m, G = keys.shape
     MT, NB = (m + 31) // 32, (G + 31) // 32
-    out = np.zeros((NB, beta, MT, 32, 32), np.uint8)
     kp = np.zeros((beta, MT * 32, NB * 32), np.uint8)
     kp[:, :m, :G] = keys
-    for gl in range(32):
-        for rr in range(32):
-            out[:, :, :, gl, rr ^ gl] = kp[:, rr::32, gl::32].transpose(2, 0, 1)
+    out = np.zeros((NB, MT, beta, 2, 32, 16), np.uint8)
+    for l in range(32):
+        for j in range(32):
+            gl = (l + j) % 32
+            # kp[i, t*32 + l, gb*32 + gl] for all (i, t, gb)
+            out[:, :, :, j >> 4, l, j & 15] = kp[:, l::32, gl::32].transpose(2, 1, 0)
     return out.reshape(-1)
 
 
@@ -222,7 +224,8 @@ def test_short_x_is_zero_padded(bq, port, cuda):
 
 
 def test_row_sharding_is_bitwise_invariant(bq, cuda):
-    """Row-sharded layers (the multi-GPU decomposition) reproduce the full y bitwise."""
+    """Row-sharded layers (the multi-GPU decomposition, shard boundaries on
+    32-row tiles) reproduce the full y bitwise."""
     w = bq.random_uniform(1000, 777, 9)
     x = bq.random_normal(777, 3, 10)
     full = bq.PackedLinear.from_weights(w, 3, 8)
@@ -230,7 +233,7 @@ def test_row_sharding_is_bitwise_invariant(bq, cuda):
     y = full.forward(x)
     y1 = full.forward(x[:, :1].copy())
     for k in (2, 3, 8):
-        bounds = [1000 * i // k for i in range(k + 1)]
+        bounds = [min(1000, 32 * ((1000 * i // k + 31) // 32)) for i in range(k + 1)]
         parts, parts1 = [], []
         for a, z in zip(bounds[:-1], bounds[1:]):
             shard = bq.PackedLinear.from_keys(keys[:, a:z], alpha[:, a:z], 777, 8)
