@@ -108,6 +108,9 @@ int bqg_bqgm_serialize(const void* h_keys, const float* h_alpha, size_t m, size_
  * d_alpha: beta x m f32.  Uses a temporary fp64 buffer of beta*m doubles. */
 int bqg_quantize_greedy_f32(const float* d_w, size_t m, size_t n, unsigned beta,
                             uint32_t* d_planes, float* d_alpha, void* stream);
+/* quantize_greedy<double>: same algorithm, double W, double alpha. */
+int bqg_quantize_greedy_f64(const double* d_w, size_t m, size_t n, unsigned beta,
+                            uint32_t* d_planes, double* d_alpha, void* stream);
 
 /* pack_keys (packing.hpp:84-107), bit-exact, for one plane.
  * d_plane: m x ceil(n/32) words.  d_keys: m x G, u8 (mu <= 8) or u16. */
@@ -123,8 +126,10 @@ int bqg_tile_keys(const uint8_t* d_keys, size_t m, size_t n, unsigned beta, unsi
  * (x_rows x b), in the reference's LutBlock layout (lut.hpp:90-97).
  *   _f32: the fast path's bank-owned shared-memory builder (mu <= 8),
  *         fp32, DP order; bit-exact with the DP evaluated in fp32.
- *   _f64: the exact path's builder, fp64, bit-exact with the reference.
- * builder must be BQG_LUT_DP (the naive builder is an oracle only).
+ *   _f64: the exact path's builder, fp64, bit-exact with the reference;
+ *         builder BQG_LUT_DP (lut.hpp:50-69) or BQG_LUT_NAIVE (lut.hpp:31-43).
+ *   _f64x: as _f64 for a double x (Matrix<double>).
+ * The _f32 builder is DP only.
  * *ops (may be NULL) receives the reference's counted ops. */
 int bqg_build_lut_f32(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0,
                       size_t count, int layout, int builder, float* d_entries, uint64_t* ops,
@@ -132,6 +137,9 @@ int bqg_build_lut_f32(const float* d_x, size_t x_rows, size_t b, unsigned mu, si
 int bqg_build_lut_f64(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0,
                       size_t count, int layout, int builder, double* d_entries, uint64_t* ops,
                       void* stream);
+int bqg_build_lut_f64x(const double* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0,
+                       size_t count, int layout, int builder, double* d_entries, uint64_t* ops,
+                       void* stream);
 
 /* The BiQGEMM multiply, biqgemm (kernel.hpp:246-258) / biqgemm_plane
  * (kernel.hpp:209-215 when d_alpha == NULL, alpha = 1):

@@ -70,10 +70,12 @@ SIGNATURES = {
     "bqg_bqgm_parse": (i32, [vp, sz, P(sz), P(sz), P(u32), P(u32), vp, vp]),
     "bqg_bqgm_serialize": (i32, [vp, vp, sz, sz, u32, u32, vp, P(sz)]),
     "bqg_quantize_greedy_f32": (i32, [vp, sz, sz, u32, vp, vp, vp]),
+    "bqg_quantize_greedy_f64": (i32, [vp, sz, sz, u32, vp, vp, vp]),
     "bqg_pack_keys": (i32, [vp, sz, sz, u32, vp, vp]),
     "bqg_tile_keys": (i32, [vp, sz, sz, u32, u32, vp, vp]),
     "bqg_build_lut_f32": (i32, [vp, sz, sz, u32, sz, sz, i32, i32, vp, P(u64), vp]),
     "bqg_build_lut_f64": (i32, [vp, sz, sz, u32, sz, sz, i32, i32, vp, P(u64), vp]),
+    "bqg_build_lut_f64x": (i32, [vp, sz, sz, u32, sz, sz, i32, i32, vp, P(u64), vp]),
     "bqg_biqgemm_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
     "bqg_biqgemm_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
     "bqg_biqgemm_exact_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),

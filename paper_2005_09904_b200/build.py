@@ -87,9 +87,27 @@ def build_oracle() -> None:
     _run(["make", "-s", "-C", str(ROOT / "oracle")])
 
 
+CPP_TEST = ROOT / "build" / "dropin_test"
+
+
+def build_cpp_tests(force: bool = False) -> Path:
+    """The reference's unit/acceptance tests re-expressed against the drop-in
+    C++ API (include/biqgemm_b200/), linked to the built library."""
+    src = ROOT / "tests" / "cpp" / "dropin_test.cpp"
+    deps = [src, LIB] + sorted((ROOT / "include" / "biqgemm_b200").glob("*.hpp")) + [ROOT / "include" / "bqg_capi.h"]
+    if force or _stale(CPP_TEST, deps):
+        CPP_TEST.parent.mkdir(parents=True, exist_ok=True)
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"), "-I", "/usr/local/cuda/include",
+              str(src), "-o", str(CPP_TEST), "-L", str(LIBDIR), "-lbiqgemm_b200", "-Wl,-rpath," + str(LIBDIR),
+              "-Wl,-rpath,$ORIGIN/../paper_2005_09904_b200/lib", "-L/usr/local/cuda/lib64", "-lcudart",
+              "-Wl,-rpath,/usr/local/cuda/lib64"])
+    return CPP_TEST
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     lib = build_library(force=force, verbose=verbose)
     build_oracle()
+    build_cpp_tests(force=force)
     return lib
 
 

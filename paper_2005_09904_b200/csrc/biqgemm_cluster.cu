@@ -107,8 +107,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             mbar_init(&empty[s], NW);
         }
         fence_mbar_init();
+        if (tl) g_timeline_c[blockIdx.x][14] = gtimer_c();
     }
     __syncthreads();
+    if (tl) g_timeline_c[blockIdx.x][15] = gtimer_c();
 
     // This CTA's slice of the cluster's outputs (row-major over rows x b).
     const int nr = max(0, min(T1 * 32, p.m) - T0 * 32);  // real rows of this cluster
@@ -127,7 +129,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                 for (int c0 = 0; c0 < cps; c0 += NW, ++sc) {
                     const int cnt = min(NW, cps - c0);
                     const int slot = sc % R;
-                    mbar_wait(&empty[slot], ((sc / R) & 1) ^ 1);
+                    if (sc >= R) mbar_wait(&empty[slot], ((sc / R) & 1) ^ 1);  // first R stages are free
+                    if ((p.debug & 2) && blockIdx.x < 8192 && sc == 0) g_timeline_c[blockIdx.x][13] = gtimer_c();
                     mbar_arrive_expect_tx(&full[slot], cnt * 1024);
                     bulk_g2s(stages + slot * STAGE_BYTES, kseg + static_cast<long long>(c0) * 1024, cnt * 1024,
                              &full[slot], pol);
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) goff[j] = lut_abs | (static_cast<uint32_t>((lane + j) & 31) * 4u * BT);
         const uint32_t lut_s = smem_u32(lut);
+        if (tl) g_timeline_c[blockIdx.x][12] = gtimer_c();
         pdl_wait();  // x (and the workspace) of the predecessor are visible from here on
         if (tl) {
             g_timeline_c[blockIdx.x][1] = gtimer_c();

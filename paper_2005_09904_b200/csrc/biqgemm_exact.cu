@@ -26,9 +26,11 @@ constexpr size_t kLutTileBudget = size_t(256) << 20;  // bytes of fp64 tables pe
 
 // One thread per (table (gl, col), k < 2^(mu-1)).  layout: 0 table-major,
 // 1 key-major, within the tile (LutBlock::index, lut.hpp:90-97).
+// naive = 0: build_lut_dp order (lut.hpp:50-69); naive = 1: build_lut_naive
+// (lut.hpp:31-43), every entry an explicit signed sum, t ascending.
 template <typename T>
 __global__ void build_lut_exact_kernel(const T* __restrict__ x, long long x_rows, long long b, int mu,
-                                       long long g0, long long count, int key_major,
+                                       long long g0, long long count, int key_major, int naive,
                                        double* __restrict__ out) {
     const long long half = 1LL << (mu - 1);
     const long long table = 1LL << mu;
@@ -53,6 +55,25 @@ __global__ void build_lut_exact_kernel(const T* __restrict__ x, long long x_rows
     }
     const long long base = gl * b * table;
     const long long kk = table - 1 - k;
+    if (naive) {
+        // both halves computed directly: acc += s_t * x_t, t ascending, from +0.0
+        double e1 = 0.0, e2 = 0.0;
+        for (int t = 0; t < mu; ++t) {
+            const long long r = g * mu + t;
+            const double xv = r < x_rows ? static_cast<double>(x[r * b + col]) : 0.0;
+            e1 = __dadd_rn(e1, __dmul_rn(((k >> t) & 1) ? 1.0 : -1.0, xv));
+            e2 = __dadd_rn(e2, __dmul_rn(((kk >> t) & 1) ? 1.0 : -1.0, xv));
+        }
+        e = e1;
+        if (key_major) {
+            out[base + k * b + col] = e1;
+            out[base + kk * b + col] = e2;
+        } else {
+            out[base + col * table + k] = e1;
+            out[base + col * table + kk] = e2;
+        }
+        return;
+    }
     if (key_major) {
         out[base + k * b + col] = e;
         out[base + kk * b + col] = -e;
@@ -114,10 +135,11 @@ size_t exact_workspace_bytes(long long m, long long n, int beta, int mu, long lo
 
 template <typename T>
 cudaError_t launch_build_lut_exact(const T* x, long long x_rows, long long b, int mu, long long g0,
-                                   long long count, bool key_major, double* out, cudaStream_t stream) {
+                                   long long count, bool key_major, double* out, cudaStream_t stream,
+                                   bool naive) {
     const long long work = count * b * (1LL << (mu - 1));
     build_lut_exact_kernel<T><<<blocks_for(work, 256), 256, 0, stream>>>(x, x_rows, b, mu, g0, count,
-                                                                        key_major ? 1 : 0, out);
+                                                                        key_major ? 1 : 0, naive ? 1 : 0, out);
     return cudaGetLastError();
 }
 
@@ -153,9 +175,9 @@ cudaError_t launch_biqgemm_exact(const void* keys, const T* alpha, const T* x, l
 }
 
 template cudaError_t launch_build_lut_exact<float>(const float*, long long, long long, int, long long,
-                                                   long long, bool, double*, cudaStream_t);
+                                                   long long, bool, double*, cudaStream_t, bool);
 template cudaError_t launch_build_lut_exact<double>(const double*, long long, long long, int, long long,
-                                                    long long, bool, double*, cudaStream_t);
+                                                    long long, bool, double*, cudaStream_t, bool);
 template cudaError_t launch_biqgemm_exact<float>(const void*, const float*, const float*, long long, float*,
                                                  long long, long long, int, int, long long, void*, size_t,
                                                  cudaStream_t);

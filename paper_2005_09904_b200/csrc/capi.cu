@@ -312,8 +312,9 @@ extern "C" int bqg_bqgm_serialize(const void* keys, const float* alpha, size_t m
 
 // ============================================================== device primitives
 
-extern "C" int bqg_quantize_greedy_f32(const float* d_w, size_t m, size_t n, unsigned beta, uint32_t* d_planes,
-                                       float* d_alpha, void* stream) {
+template <typename T>
+static int quantize_impl(const T* d_w, size_t m, size_t n, unsigned beta, uint32_t* d_planes, T* d_alpha,
+                         void* stream) {
     // quantize.hpp:29-31
     if (beta == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "quantize_greedy: beta must be >= 1");
     int s = check_dims(m, n, "quantize_greedy");
@@ -323,11 +324,21 @@ extern "C" int bqg_quantize_greedy_f32(const float* d_w, size_t m, size_t n, uns
     cudaStream_t st = as_stream(stream);
     double* alpha_d = nullptr;
     BQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&alpha_d), sizeof(double) * beta * m, st));
-    cudaError_t e = bqg::launch_quantize_greedy(d_w, static_cast<long long>(m), static_cast<long long>(n),
-                                                static_cast<int>(beta), d_planes, d_alpha, alpha_d, st);
+    cudaError_t e = bqg::launch_quantize_greedy<T>(d_w, static_cast<long long>(m), static_cast<long long>(n),
+                                                   static_cast<int>(beta), d_planes, d_alpha, alpha_d, st);
     cudaFreeAsync(alpha_d, st);
     if (e != cudaSuccess) return cuda_err(e, "quantize_greedy kernel");
     return BQG_OK;
+}
+
+extern "C" int bqg_quantize_greedy_f32(const float* d_w, size_t m, size_t n, unsigned beta, uint32_t* d_planes,
+                                       float* d_alpha, void* stream) {
+    return quantize_impl<float>(d_w, m, n, beta, d_planes, d_alpha, stream);
+}
+
+extern "C" int bqg_quantize_greedy_f64(const double* d_w, size_t m, size_t n, unsigned beta, uint32_t* d_planes,
+                                       double* d_alpha, void* stream) {
+    return quantize_impl<double>(d_w, m, n, beta, d_planes, d_alpha, stream);
 }
 
 extern "C" int bqg_pack_keys(const uint32_t* d_plane, size_t m, size_t n, unsigned mu, void* d_keys, void* stream) {
@@ -358,15 +369,16 @@ extern "C" int bqg_tile_keys(const uint8_t* d_keys, size_t m, size_t n, unsigned
 }
 
 namespace {
-int check_lut_args(size_t x_rows, size_t b, unsigned mu, size_t count, int layout, int builder, const char* who) {
+int check_lut_args(size_t x_rows, size_t b, unsigned mu, size_t count, int layout, int builder, const char* who,
+                   bool allow_naive = false) {
     int s = check_mu(mu, who);
     if (s) return s;
     if (count == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "build_lut_block: empty tile");  // lut.hpp:114-116
     if (x_rows == 0 || b == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: x dimensions must be nonzero", who);
     if (layout != BQG_LUT_TABLE_MAJOR && layout != BQG_LUT_KEY_MAJOR)
         return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: unknown layout", who);
-    if (builder != BQG_LUT_DP)
-        return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: only the DP builder runs on the device", who);
+    if (builder != BQG_LUT_DP && !(allow_naive && builder == BQG_LUT_NAIVE))
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: unsupported builder", who);
     return BQG_OK;
 }
 }  // namespace
@@ -386,18 +398,36 @@ extern "C" int bqg_build_lut_f32(const float* d_x, size_t x_rows, size_t b, unsi
     return BQG_OK;
 }
 
-extern "C" int bqg_build_lut_f64(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0, size_t count,
-                                 int layout, int builder, double* d_entries, uint64_t* ops, void* stream) {
-    int s = check_lut_args(x_rows, b, mu, count, layout, builder, "build_lut_f64");
+template <typename T>
+static int build_lut_exact_impl(const T* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0, size_t count,
+                                int layout, int builder, double* d_entries, uint64_t* ops, void* stream,
+                                const char* who) {
+    int s = check_lut_args(x_rows, b, mu, count, layout, builder, who, true);
     if (s) return s;
+    if (!d_x || !d_entries) return set_err(BQG_ERR_INVALID_ARGUMENT, "%s: null pointer", who);
     BQG_NEED_DEVICE();
-    cudaError_t e = bqg::launch_build_lut_exact<float>(
+    cudaError_t e = bqg::launch_build_lut_exact<T>(
         d_x, static_cast<long long>(x_rows), static_cast<long long>(b), static_cast<int>(mu),
         static_cast<long long>(g0), static_cast<long long>(count), layout == BQG_LUT_KEY_MAJOR, d_entries,
-        as_stream(stream));
-    if (e != cudaSuccess) return cuda_err(e, "build_lut_f64 kernel");
-    if (ops) *ops += ((uint64_t(1) << mu) + mu - 1) * count * b;
+        as_stream(stream), builder == BQG_LUT_NAIVE);
+    if (e != cudaSuccess) return cuda_err(e, "build_lut exact kernel");
+    // lut.hpp:42 (naive: 2^mu * mu per table), lut.hpp:68 (dp: 2^mu + mu - 1)
+    const uint64_t per = builder == BQG_LUT_NAIVE ? (uint64_t(1) << mu) * mu : (uint64_t(1) << mu) + mu - 1;
+    if (ops) *ops += per * count * b;
     return BQG_OK;
+}
+
+extern "C" int bqg_build_lut_f64(const float* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0, size_t count,
+                                 int layout, int builder, double* d_entries, uint64_t* ops, void* stream) {
+    return build_lut_exact_impl<float>(d_x, x_rows, b, mu, g0, count, layout, builder, d_entries, ops, stream,
+                                       "build_lut_f64");
+}
+
+extern "C" int bqg_build_lut_f64x(const double* d_x, size_t x_rows, size_t b, unsigned mu, size_t g0,
+                                  size_t count, int layout, int builder, double* d_entries, uint64_t* ops,
+                                  void* stream) {
+    return build_lut_exact_impl<double>(d_x, x_rows, b, mu, g0, count, layout, builder, d_entries, ops, stream,
+                                        "build_lut_f64x");
 }
 
 extern "C" size_t bqg_biqgemm_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu) {

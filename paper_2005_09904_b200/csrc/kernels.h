@@ -42,8 +42,9 @@ size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b
 // Grid planner: CTAs per 32-group block.
 int plan_cpb(long long m, long long groups, int beta, long long b, int num_sms);
 
-cudaError_t launch_quantize_greedy(const float* w, long long m, long long n, int beta,
-                                   uint32_t* planes, float* alpha, double* alpha_d,
+template <typename T>
+cudaError_t launch_quantize_greedy(const T* w, long long m, long long n, int beta,
+                                   uint32_t* planes, T* alpha, double* alpha_d,
                                    cudaStream_t stream);
 cudaError_t launch_pack_keys(const uint32_t* plane, long long m, long long n, int mu, void* keys,
                              cudaStream_t stream);
@@ -68,7 +69,7 @@ cudaError_t launch_build_lut_f32(const float* x, long long x_rows, long long b, 
 template <typename T>
 cudaError_t launch_build_lut_exact(const T* x, long long x_rows, long long b, int mu, long long g0,
                                    long long count, bool key_major, double* out,
-                                   cudaStream_t stream);
+                                   cudaStream_t stream, bool naive = false);
 template <typename T>
 cudaError_t launch_biqgemm_exact(const void* keys_rowmajor, const T* alpha, const T* x,
                                  long long x_rows, T* y, long long m, long long n, int beta,

@@ -20,18 +20,19 @@ namespace {
 
 constexpr int kQWarps = 4;  // warps per CTA; each warp owns 32 rows
 
+template <typename T>
 __global__ void __launch_bounds__(kQWarps * 32)
-    quantize_greedy_kernel(const float* __restrict__ w, long long m, long long n, int beta,
-                           uint32_t* __restrict__ planes, float* __restrict__ alpha,
+    quantize_greedy_kernel(const T* __restrict__ w, long long m, long long n, int beta,
+                           uint32_t* __restrict__ planes, T* __restrict__ alpha,
                            double* __restrict__ alpha_d) {
-    __shared__ float tile[kQWarps][32][33];
+    __shared__ T tile[kQWarps][32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long r0 = (static_cast<long long>(blockIdx.x) * kQWarps + warp) * 32;
     if (r0 >= m) return;
     const long long r = r0 + lane;
     const bool row_ok = r < m;
     const long long wpr = (n + 31) / 32;
-    float(*t)[33] = tile[warp];
+    T(*t)[33] = tile[warp];
 
     for (int i = 0; i < beta; ++i) {
         // pass A: alpha_i = (sequential sum |res_i|) / n
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(kQWarps * 32)
 #pragma unroll 4
             for (int rr = 0; rr < 32; ++rr) {
                 const long long rg = r0 + rr, c = c0 + lane;
-                t[rr][lane] = (rg < m && c < n) ? w[rg * n + c] : 0.0f;
+                t[rr][lane] = (rg < m && c < n) ? w[rg * n + c] : T(0);
             }
             __syncwarp();
             if (row_ok) {
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(kQWarps * 32)
         if (row_ok) {
             a = __ddiv_rn(abs_sum, static_cast<double>(n));
             alpha_d[static_cast<long long>(i) * m + r] = a;
-            alpha[static_cast<long long>(i) * m + r] = __double2float_rn(a);
+            alpha[static_cast<long long>(i) * m + r] = static_cast<T>(a);  // T(alpha), round to nearest
         }
         // pass B: sign bits of res_i (sign(0) = +1, quantize.hpp:51)
         for (long long c0 = 0; c0 < n; c0 += 32) {
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(kQWarps * 32)
 #pragma unroll 4
             for (int rr = 0; rr < 32; ++rr) {
                 const long long rg = r0 + rr, c = c0 + lane;
-                t[rr][lane] = (rg < m && c < n) ? w[rg * n + c] : 0.0f;
+                t[rr][lane] = (rg < m && c < n) ? w[rg * n + c] : T(0);
             }
             __syncwarp();
             if (row_ok) {
@@ -135,14 +136,19 @@ __global__ void tile_keys_kernel(const uint8_t* __restrict__ keys, long long m, 
 
 }  // namespace
 
-cudaError_t launch_quantize_greedy(const float* w, long long m, long long n, int beta,
-                                   uint32_t* planes, float* alpha, double* alpha_d,
+template <typename T>
+cudaError_t launch_quantize_greedy(const T* w, long long m, long long n, int beta,
+                                   uint32_t* planes, T* alpha, double* alpha_d,
                                    cudaStream_t stream) {
     const long long rows_per_cta = kQWarps * 32;
     const unsigned grid = static_cast<unsigned>((m + rows_per_cta - 1) / rows_per_cta);
-    quantize_greedy_kernel<<<grid, kQWarps * 32, 0, stream>>>(w, m, n, beta, planes, alpha, alpha_d);
+    quantize_greedy_kernel<T><<<grid, kQWarps * 32, 0, stream>>>(w, m, n, beta, planes, alpha, alpha_d);
     return cudaGetLastError();
 }
+template cudaError_t launch_quantize_greedy<float>(const float*, long long, long long, int, uint32_t*, float*,
+                                                   double*, cudaStream_t);
+template cudaError_t launch_quantize_greedy<double>(const double*, long long, long long, int, uint32_t*, double*,
+                                                    double*, cudaStream_t);
 
 cudaError_t launch_pack_keys(const uint32_t* plane, long long m, long long n, int mu,
                              void* keys, cudaStream_t stream) {

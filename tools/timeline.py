@@ -47,7 +47,8 @@ if CLUSTER:
              ("d barrier", t[:, 6] - t[:, 4]), ("d reduce", t[:, 5] - t[:, 6])]
 if CLUSTER and int(os.environ["BQG_DEBUG_FLAGS"]) & 1024:
     rows += [("lat x", t[:, 8]), ("lat keys", t[:, 9]), ("lat alpha", t[:, 10]), ("lat partial", t[:, 11])]
-if CLUSTER and int(os.environ["BQG_DEBUG_FLAGS"]) & 64:
-    rows += [("rebuild", t[:, 12] - t[:, 2])]
+if CLUSTER:
+    rows += [("bar_init", t[:, 14] - t0), ("syncthreads", t[:, 15] - t0), ("tma_issue0", t[:, 13] - t0),
+             ("pre_pdlwait", t[:, 12] - t0)]
 for name, v in rows:
     print(f"{name:12s} min {v.min():7d} med {int(np.median(v)):7d} max {v.max():7d} ns")
