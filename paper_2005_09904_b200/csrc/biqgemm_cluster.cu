@@ -79,6 +79,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     };
     unsigned char* stages = place(STAGE_AREA);
     float* psum = reinterpret_cast<float*>(place(kPSUM));
+    float* xs = reinterpret_cast<float*>(place(32 * MU * BT * 4));  // staged x tile of the current segment
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + R * STAGE_BYTES);
     uint64_t* empty = full + R;
 
@@ -165,19 +166,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             const int bi = sg - ct * nblk;
             const int gb = rank + bi * cs;
             const bool first = bi == 0;  // first group block of this rank for this column tile
-            if (sg != 0) named_bar_sync(1, NW * 32);  // previous segment done with the LUT
-            build_bank_owned_tables<MU, NW, BT, LutGeom<BT>::KROW>(lut, p.x, p.x_rows, p.b,
-                                                                   static_cast<long long>(gb) * 32 + lane,
-                                                                   static_cast<long long>(ct) * BT, warp, lane);
+            if (sg != 0) named_bar_sync(1, NW * 32);  // previous segment done with the LUT and x tile
+            stage_x_tile<MU, BT>(xs, p.x, p.x_rows, p.b, gb, static_cast<long long>(ct) * BT, threadIdx.x, NW * 32);
+            named_bar_sync(1, NW * 32);
+            build_bank_owned_tables_smem<MU, NW, BT, LutGeom<BT>::KROW>(lut, xs, warp, lane);
             named_bar_sync(1, NW * 32);
             if (tl && sg == 0) g_timeline_c[blockIdx.x][2] = gtimer_c();
-            if ((p.debug & 64) && sg == 0) {  // profiling: rebuild with warm code/data, time it
-                build_bank_owned_tables<MU, NW, BT, LutGeom<BT>::KROW>(lut, p.x, p.x_rows, p.b,
-                                                                       static_cast<long long>(gb) * 32 + lane,
-                                                                       static_cast<long long>(ct) * BT, warp, lane);
-                named_bar_sync(1, NW * 32);
-                if (tl) g_timeline_c[blockIdx.x][12] = gtimer_c();
-            }
             int ti = warp / beta, ii = warp - (warp / beta) * beta;
             for (int c0 = 0; c0 < cps; c0 += NW, ++sc) {
                 const int slot = sc % R;
@@ -317,7 +311,7 @@ size_t cluster_smem_bytes() {
     const size_t lut = static_cast<size_t>(1u << MU) * LutGeom<BT>::KROW * 4;
     const size_t stages = static_cast<size_t>(kCR) * kCNW * 1024 + 2 * kCR * sizeof(uint64_t);
     // BT <= 2 aligns the LUT to 64 KiB inside the allocation (<= 64 KiB - 1 slack)
-    return (LutGeom<BT>::PRMT ? 65535 : 0) + lut + stages + kPSUM;
+    return (LutGeom<BT>::PRMT ? 65535 : 0) + lut + stages + kPSUM + 32 * MU * BT * 4;
 }
 
 template <int MU, int BT>

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     unsigned char* stages = smem + LUT_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + R * STAGE_BYTES);
     uint64_t* empty = full + R;
+    float* xs = reinterpret_cast<float*>(empty + R);  // staged x tile (32*MU x BT)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool tl = (p.debug & 2) && threadIdx.x == 0 && blockIdx.x < 8192;
@@ -152,10 +153,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
         const int pbase = pair * plan.cpp;
         const int seg_end = min(cend, pbase + plan.cpp);
         const int gb = pair / plan.CT, ct = pair - gb * plan.CT;
-        if (seg != cbeg) named_bar_sync(1, NW * 32);  // previous segment done with the LUT
-        build_bank_owned_tables<MU, NW, BT, LutGeom<BT>::KROW>(lut, p.x, p.x_rows, p.b,
-                                                               static_cast<long long>(gb) * 32 + lane,
-                                                               static_cast<long long>(ct) * BT, warp, lane);
+        if (seg != cbeg) named_bar_sync(1, NW * 32);  // previous segment done with the LUT and x tile
+        stage_x_tile<MU, BT>(xs, p.x, p.x_rows, p.b, gb, static_cast<long long>(ct) * BT, threadIdx.x, NW * 32);
+        named_bar_sync(1, NW * 32);
+        build_bank_owned_tables_smem<MU, NW, BT, LutGeom<BT>::KROW>(lut, xs, warp, lane);
         named_bar_sync(1, NW * 32);
         if (tl) g_timeline[blockIdx.x][2] = gtimer();
 
@@ -248,7 +249,7 @@ constexpr int stages_for() {
 template <int MU, int BT>
 size_t smem_bytes() {
     return static_cast<size_t>(1u << MU) * LutGeom<BT>::KROW * 4 + static_cast<size_t>(stages_for<BT>()) * kNW * 1024 +
-           2 * stages_for<BT>() * sizeof(uint64_t);
+           2 * stages_for<BT>() * sizeof(uint64_t) + 32 * MU * BT * 4;
 }
 
 template <int MU, int BT>
@@ -367,7 +368,11 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
     }
     QueryParams p = p_in;
     p.debug = debug_flags;
-    if (!(debug_flags & 128)) {  // 128: force the two-kernel form (profiling)
+    // The single-kernel cluster form wins when the per-call fixed costs
+    // dominate and one column tile covers b (measured: C2 6.6 vs 8.5 us); the
+    // two-kernel form (148 CTAs, cost-model split) wins for larger b / m.
+    const bool cluster_shape = p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
+    if (!(debug_flags & 128) && (cluster_shape || (debug_flags & 8192))) {  // 128/8192: force a form (profiling)
         bool used = false;
         cudaError_t e = launch_biqgemm_cluster(p, mu, pdl, stream, &used);
         if (e != cudaSuccess || used) return e;

@@ -153,4 +153,68 @@ __device__ __forceinline__ void build_bank_owned_tables(float* lut, const float*
     }
 }
 
+// x staged once per CTA: xs[(rl)*BT + c] = x(gb*32*MU + rl, col0 + c) for the
+// block's 32*MU input rows (0 past x_rows or past b).  Coalesced cooperative
+// load by `nthreads` threads; caller synchronises before the build.
+template <int MU, int BT>
+__device__ __forceinline__ void stage_x_tile(float* xs, const float* __restrict__ x, long long x_rows, long long b,
+                                             long long gb, long long col0, int tid, int nthreads) {
+    const long long r0 = gb * 32 * MU;
+    for (int idx = tid; idx < 32 * MU * BT; idx += nthreads) {
+        const int rl = idx / BT, c = idx - (idx / BT) * BT;
+        const long long r = r0 + rl, col = col0 + c;
+        xs[idx] = (r < x_rows && col < b) ? __ldcg(x + r * b + col) : 0.0f;
+    }
+}
+
+// build_bank_owned_tables with x read from the staged shared-memory tile
+// (identical arithmetic and order; lane l owns group gb*32 + l).
+template <int MU, int NW, int BT, int KROW = 32 * BT>
+__device__ __forceinline__ void build_bank_owned_tables_smem(float* lut, const float* xs, int warp, int lane) {
+    constexpr int L = (MU - 1) < 2 ? (MU - 1) : 2;
+    constexpr int NCH = 1 << (MU - 1 - L);
+    constexpr int TABLE = 1 << MU;
+    if (warp >= NCH) return;
+    float xv[MU][BT];
+#pragma unroll
+    for (int t = 0; t < MU; ++t)
+#pragma unroll
+        for (int c = 0; c < BT; ++c) xv[t][c] = xs[(lane * MU + t) * BT + c];
+    float low[1 << L][BT];
+#pragma unroll
+    for (int c = 0; c < BT; ++c) {
+        float e0 = 0.0f;
+#pragma unroll
+        for (int t = 0; t < MU; ++t) e0 = __fsub_rn(e0, xv[t][c]);
+        low[0][c] = e0;
+#pragma unroll
+        for (int i = 1; i <= L; ++i) {
+            const float step = 2.0f * xv[i - 1][c];
+            const int half = 1 << (i - 1);
+#pragma unroll
+            for (int j = 0; j < half; ++j) low[j + half][c] = fadd_rn(low[j][c], step);
+        }
+    }
+#pragma unroll 1
+    for (int ch = warp; ch < NCH; ch += NW) {
+#pragma unroll
+        for (int j = 0; j < (1 << L); ++j) {
+            float v[BT];
+#pragma unroll
+            for (int c = 0; c < BT; ++c) {
+                float e = low[j][c];
+#pragma unroll
+                for (int t = L; t < MU - 1; ++t) {
+                    const float st = 2.0f * xv[t][c];
+                    e = ((ch >> (t - L)) & 1) ? fadd_rn(e, st) : e;
+                }
+                v[c] = e;
+            }
+            const int k = (ch << L) + j;
+            store_vec<BT>(lut + k * KROW + lane * BT, v, false);
+            store_vec<BT>(lut + (TABLE - 1 - k) * KROW + lane * BT, v, true);
+        }
+    }
+}
+
 }  // namespace bqg
