@@ -350,3 +350,17 @@ def test_baseline_configs(bq, cuda, name):
     y = layer.forward(x)
     assert_close(y, y_exact)
     layer.close()
+
+
+@pytest.mark.parametrize("flags", ["8192", "128"])
+def test_both_fast_forms(cuda, flags):
+    """Force each fast-path form (single-kernel cluster / two-kernel) on
+    assorted shapes in a subprocess (the form switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, BQG_DEBUG_FLAGS=flags)
+    r = subprocess.run([sys.executable, str(Path(__file__).parent / "forms_check.py")], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
