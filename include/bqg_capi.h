@@ -158,6 +158,30 @@ int bqg_biqgemm_f32(const uint8_t* d_keys_tiled, const float* d_alpha, const flo
                     size_t x_rows, float* d_y, size_t m, size_t n, size_t b, unsigned beta,
                     unsigned mu, void* d_workspace, size_t workspace_bytes, int pdl, void* stream);
 
+/* Grouped calls: `count` independent biqgemm calls (kernel.hpp:246-258, one
+ * per entry) that share (m, n, b, beta, mu) but have their own weights,
+ * alpha, x and y -- the Q/K/V or gate/up projections of one layer, or one
+ * GEMV per request of a serving batch.  Equivalent to calling
+ * bqg_biqgemm_f32 once per entry; the difference is only on the device:
+ * for b == 1, mu == 8, beta <= 4 the calls run in ONE persistent kernel
+ * whose key stream runs ahead across call boundaries (no per-call kernel
+ * handoff), followed by one fixed-order epilogue kernel.  Other shapes run
+ * the single-call kernels back to back.  h_calls is a HOST array (copied
+ * into the launch; graph-capturable); entries' device pointers must stay
+ * valid until the stream reaches the work.  y is bitwise identical to the
+ * single-call stream form and deterministic. */
+typedef struct bqg_call {
+    const uint8_t* d_keys_tiled;
+    const float* d_alpha; /* NULL = plane mode (alpha = 1) */
+    const float* d_x;
+    float* d_y;
+} bqg_call;
+size_t bqg_biqgemm_grouped_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                           size_t count);
+int bqg_biqgemm_grouped_f32(const bqg_call* h_calls, size_t count, size_t x_rows, size_t m, size_t n,
+                            size_t b, unsigned beta, unsigned mu, void* d_workspace,
+                            size_t workspace_bytes, int pdl, void* stream);
+
 /* Exact path: any mu in 1..16, any b; d_keys ROW-MAJOR (beta x m x G, u8 for
  * mu <= 8 else u16); fp64 LUT and accumulation in the reference's order, so y
  * is bit-identical to the reference.  Workspace from

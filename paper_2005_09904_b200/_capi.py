@@ -54,6 +54,12 @@ class KernelStats(C.Structure):
     ]
 
 
+class Call(C.Structure):
+    """bqg_call: one entry of a grouped biqgemm launch."""
+
+    _fields_ = [("d_keys_tiled", vp), ("d_alpha", vp), ("d_x", vp), ("d_y", vp)]
+
+
 # name -> (restype, argtypes).  Every symbol declared in include/bqg_capi.h.
 SIGNATURES = {
     "bqg_status_string": (C.c_char_p, [i32]),
@@ -78,6 +84,8 @@ SIGNATURES = {
     "bqg_build_lut_f64x": (i32, [vp, sz, sz, u32, sz, sz, i32, i32, vp, P(u64), vp]),
     "bqg_biqgemm_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
     "bqg_biqgemm_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
+    "bqg_biqgemm_grouped_workspace_bytes": (sz, [sz, sz, sz, u32, u32, sz]),
+    "bqg_biqgemm_grouped_f32": (i32, [vp, sz, sz, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
     "bqg_biqgemm_exact_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
     "bqg_biqgemm_exact_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),
     "bqg_biqgemm_exact_f64": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),

@@ -222,6 +222,27 @@ def biqgemm_device(tiled, alpha, x, y, m, n, beta, mu, workspace: Workspace, pdl
     return y
 
 
+def grouped_workspace(m, n, b, beta, mu, count, device="cuda") -> Workspace:
+    return Workspace(int(lib.bqg_biqgemm_grouped_workspace_bytes(m, n, b, beta, mu, count)), device=device)
+
+
+def make_calls(entries):
+    """Host array of bqg_call from (tiled, alpha|None, x, y) device-tensor tuples."""
+    arr = (_capi.Call * len(entries))()
+    for i, (t, a, x, y) in enumerate(entries):
+        arr[i] = _capi.Call(_ptr(t), _ptr(a) if a is not None else None, _ptr(x), _ptr(y))
+    return arr
+
+
+def biqgemm_grouped_device(calls, x_rows, m, n, b, beta, mu, workspace: Workspace, pdl=False, stream=None):
+    """`len(calls)` independent fast-path calls (tiled keys, alpha, x, y per entry) in one grouped launch.
+    `calls` is a make_calls() array or a list of tuples."""
+    if not isinstance(calls, C.Array):
+        calls = make_calls(calls)
+    check(lib.bqg_biqgemm_grouped_f32(C.cast(calls, C.c_void_p), len(calls), x_rows, m, n, b, beta, mu,
+                                      workspace.ptr(), workspace.nbytes, 1 if pdl else 0, _stream(stream)))
+
+
 def biqgemm_exact_device(keys, alpha, x, y, m, n, beta, mu, stream=None):
     """Exact path (fp64, bit-identical to the reference) on device tensors; keys row-major."""
     x_rows, b = x.shape

@@ -1,0 +1,466 @@
+// biqgemm_stream.cu -- the grouped ("stream") BiQGEMM form: b == 1, mu == 8,
+// 1 <= beta <= 4, for a GROUP of independent calls that share (m, n, beta,
+// mu) -- e.g. the Q/K/V or gate/up projections of one layer, or the
+// per-request GEMVs of a serving batch.  Each call is a full
+// biqgemm::biqgemm (/root/reference/proj/core/include/biqgemm/kernel.hpp:
+// 246-258 -> detail::run 116-204): its own x, its own LUT build
+// (lut.hpp:50-69,109-154), its own key stream and alpha epilogue
+// (kernel.hpp:183-195).  Nothing is shared or skipped between calls; the
+// group exists so that consecutive calls overlap on the device instead of
+// paying a kernel boundary (~1 us of handoff, tools/ubench/pdl_overlap.cu)
+// each.
+//
+// Work split.  A call's keys are NB x MT "units" (unit = one 32-group block
+// x one 32-row tile x all beta planes = beta KiB of the tiled layout, and
+// unit u = gb*MT + t sits at byte u*beta*1024: kernels.h).  CTA c owns the
+// contiguous unit range [c*W/grid, (c+1)*W/grid) of EVERY call (W = NB*MT,
+// grid >= NB so a range spans at most two group blocks).  Per CTA:
+//
+//   key warp   : one lane streams the CTA's unit range of call 0, 1, 2, ...
+//                global -> shared with cp.async.bulk (TMA bulk engine,
+//                L2::evict_first) through an R-stage mbarrier ring that
+//                runs ahead across call boundaries -- HBM never waits for a
+//                call boundary.
+//   x warp     : loads x of call c+1 (the <= 2 blocks' 256 rows each) into a
+//                double-buffered shared tile one call ahead.
+//   15 consumer warps, per call c:
+//       one named barrier (everybody is done with call c-1 and LUT(c) is
+//       complete), build their share of LUT(c+1) into the other of two
+//       64 KiB LUT buffers (bank-owned DP tables, bit-exact with the fp32
+//       DP, lut_build.cuh), then gather their units of call c: lane l = row
+//       l of the tile, step j reads table (l+j) mod 32 -> one conflict-free
+//       wavefront per 32 lookups; address = ONE PRMT (key byte -> bits
+//       8..15, rotated bank -> bits 2..6, buffer base -> bits 16..31; the
+//       second block of a CTA that spans two sits at +128 B, an LDS
+//       immediate).  Per unit the beta plane sums are combined with alpha in
+//       fp64 and stored as ONE fp32 partial per (call, block, row).
+//   stream_finalize_kernel (PDL-chained): y_c[r] = sum over blocks (fp64,
+//       blocks ascending) -> f32.
+//
+// Every output's reduction tree is a function of (n, mu) only (gather order
+// within a block, planes ascending, blocks ascending), so y is bitwise
+// independent of the grid, the group size and any 32-row-aligned row
+// sharding.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bqg {
+
+namespace {
+
+constexpr int kMU = 8;
+constexpr int kTable = 1 << kMU;
+constexpr int kNC = 14;                          // consumer (gather) warps
+constexpr int kWKey = kNC, kWLoad = kNC + 1;     // key-stream warp, x/alpha loader warp
+constexpr int kWBuild = kNC + 2;                 // two LUT builder warps
+constexpr int kSThreads = (kNC + 4) * 32;
+constexpr int kMaxStages = 24;
+constexpr int kStreamSmem = 227 * 1024;          // opt-in maximum per CTA
+constexpr int kXBlock = 32 * kMU;                // x rows per group block
+constexpr int kAlphaBudget = 48 * 1024;          // both alpha buffers together
+
+struct StreamArgs {
+    int ncalls;
+    long long x_rows;
+    int m, NB, MT, cpb, grid, ups;
+    float* partial;  // ncalls x NB x (MT*32), fp32
+    StreamCall calls[kStreamMaxGroup];
+};
+
+// ---------------------------------------------------------------- LUT build
+// The table of group gb*32 + lane lives in bank `lane`: entry k of buffer
+// half h at byte  base + k*256 + h*128 + lane*4.  The first half (keys <
+// 128) is the DP recurrence of lut.hpp:50-69 evaluated in fp32,
+//     e[0] = ((0 - x0) - x1) - ... - x7,   e[k] = e[k - 2^top(k)] + 2*x_top(k),
+// and the second half its negation, e[255 - k] = -e[k] (lut.hpp:63-66).  The
+// recurrence tree is walked depth-first at compile time (parent -> child =
+// one fadd), so every entry is produced by exactly the reference's addition
+// and the live state is one value per tree level.
+//   builder 0: keys with bit 6 clear (64 entries + their complements);
+//   builder 1: keys with bit 6 set, e[j | 64] = e[j] + 2*x6 (it re-walks the
+//              j < 64 subtree without storing it).
+__device__ __forceinline__ void sts_pair(uint32_t col, int k, float v) {
+    sts_f32(col + static_cast<uint32_t>(k) * 256u, v);
+    sts_f32(col + static_cast<uint32_t>(kTable - 1 - k) * 256u, -v);
+}
+
+template <int K, int I, bool HI>
+struct Dfs {
+    // the children of node K through bits I .. 5
+    static __device__ __forceinline__ void children(float v, const float (&s)[kMU], uint32_t col) {
+        if constexpr (I < 6) {
+            Dfs<(K | (1 << I)), I + 1, HI>::node(fadd_rn(v, s[I]), s, col);
+            Dfs<K, I + 1, HI>::children(v, s, col);
+        }
+    }
+    static __device__ __forceinline__ void node(float v, const float (&s)[kMU], uint32_t col) {
+        if constexpr (HI) {
+            sts_pair(col, K | 64, fadd_rn(v, s[6]));
+        } else {
+            sts_pair(col, K, v);
+        }
+        children(v, s, col);
+    }
+};
+
+__device__ __forceinline__ void build_tables(int which, uint32_t col, const float* xb, int lane) {
+    float x[kMU], s[kMU];
+#pragma unroll
+    for (int t = 0; t < kMU; ++t) x[t] = xb[lane * kMU + t];
+    float e0 = 0.0f;
+#pragma unroll
+    for (int t = 0; t < kMU; ++t) e0 = __fsub_rn(e0, x[t]);
+#pragma unroll
+    for (int t = 0; t < kMU; ++t) s[t] = 2.0f * x[t];
+    if (which == 0) {
+        Dfs<0, 0, false>::node(e0, s, col);
+    } else {
+        Dfs<0, 0, true>::node(e0, s, col);
+    }
+}
+
+// ---------------------------------------------------------------- gather
+// One 1 KiB chunk (32 rows x 32 groups of one plane): lane l sums its row's
+// 32 lookups (4 interleaved accumulators combined pairwise, the order of
+// gather_chunk in query_core.cuh).  IMM selects the buffer half (+128 B).
+template <int IMM>
+__device__ __forceinline__ float stream_gather(const uint32_t (&w)[8], const uint32_t (&goff)[32]) {
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t off = __byte_perm(goff[j], w[j >> 2], 0x3200u | ((4u + (j & 3)) << 4));
+        float e;
+        asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off), "n"(IMM));
+        acc[j & 3] += e;
+    }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// beta chunks of one unit, combined with alpha in fp64 (planes ascending).
+template <int BETA, int IMM>
+__device__ __forceinline__ double stream_unit(uint32_t kbase, int lane, const uint32_t (&goff)[32],
+                                              const float (&a)[BETA]) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < BETA; ++i) {
+        uint32_t w[8];
+        const uint32_t p = kbase + static_cast<uint32_t>(i) * 1024u + static_cast<uint32_t>(lane) * 16u;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(p));
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+512];" : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "r"(p));
+        const float P = stream_gather<IMM>(w, goff);
+        s += static_cast<double>(a[i]) * static_cast<double>(P);
+    }
+    return s;
+}
+
+template <int BETA>
+__global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __grid_constant__ StreamArgs A) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    pdl_launch_dependents();
+
+    // ---- this CTA's work: tiles [t0, t0+U) of group block gb, every call
+    const int gb = blockIdx.x / A.cpb, jb = blockIdx.x - gb * A.cpb;
+    const int t0 = static_cast<int>(static_cast<long long>(jb) * A.MT / A.cpb);
+    const int U = static_cast<int>(static_cast<long long>(jb + 1) * A.MT / A.cpb) - t0;
+    const long long u0 = static_cast<long long>(gb) * A.MT + t0;
+    const int ncalls = A.ncalls;
+    const long long total_units = static_cast<long long>(ncalls) * U;
+    const uint32_t abuf_bytes = static_cast<uint32_t>(U) * BETA * 128u;
+    const bool alpha_smem = 2u * abuf_bytes <= static_cast<uint32_t>(kAlphaBudget);
+
+    // ---- shared memory: [bars | x bufs | alpha bufs | stages.. | LUT 64K | ..stages]
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t lut_abs = (sbase + 0xFFFFu) & ~0xFFFFu;
+    const uint32_t send = sbase + kStreamSmem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kMaxStages;
+    uint64_t* xfull = empty + kMaxStages;  // [2] x(c) loaded          (32 loader lanes)
+    uint64_t* xempty = xfull + 2;          // [2] x(c) consumed         (2 builders)
+    uint64_t* afull = xempty + 2;          // [2] alpha(c) loaded       (32 loader lanes)
+    uint64_t* lfull = afull + 2;           // [2] LUT(c) built          (2 builders)
+    uint64_t* lempty = lfull + 2;          // [2] call c fully gathered (kNC consumers)
+    float* xs = reinterpret_cast<float*>(smem + 1024);                    // [2][kXBlock]
+    float* as = reinterpret_cast<float*>(smem + 1024 + 2 * kXBlock * 4);  // [2][BETA][U*32]
+    const uint32_t stage_bytes = static_cast<uint32_t>(A.ups) * BETA * 1024u;
+    const uint32_t lo0 = (sbase + 1024u + 2u * kXBlock * 4u + (alpha_smem ? 2u * abuf_bytes : 0u) + 127u) & ~127u;
+    const int nlo = lo0 + stage_bytes <= lut_abs ? static_cast<int>((lut_abs - lo0) / stage_bytes) : 0;
+    const uint32_t hi0 = lut_abs + 0x10000u;
+    const int nhi = hi0 + stage_bytes <= send ? static_cast<int>((send - hi0) / stage_bytes) : 0;
+    const int nst = min(kMaxStages, nlo + nhi);
+    if (lut_abs + 0x10000u > send || nst < 2) __trap();  // layout assumption (dynamic smem starts near 0)
+    auto stage_addr = [&](int slot) -> uint32_t {
+        return slot < nlo ? lo0 + static_cast<uint32_t>(slot) * stage_bytes
+                          : hi0 + static_cast<uint32_t>(slot - nlo) * stage_bytes;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMaxStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], A.ups);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&xfull[b], 32);
+            mbar_init(&xempty[b], 2);
+            mbar_init(&afull[b], 32);
+            mbar_init(&lfull[b], 2);
+            mbar_init(&lempty[b], kNC);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kWKey) {
+        // ---------------------------------------------------- key stream
+        // Lane L owns ring slot L (stages L, L+nst, ...): the bulk copies of
+        // different stages are issued by different lanes, in parallel (one
+        // issuing thread caps the copy rate at ~3 TB/s chip-wide with 8-12
+        // KiB copies; several reach ~7 TB/s: tools/ubench/tma_stream.cu).
+        if (lane < nst) {
+            const uint64_t pol = policy_evict_first();
+            const long long nstages_total = (total_units + A.ups - 1) / A.ups;
+            for (long long s = lane; s < nstages_total; s += nst) {
+                const int slot = lane;
+                const long long round = s / nst;
+                if (round > 0) mbar_wait(&empty[slot], static_cast<uint32_t>((round - 1) & 1));
+                const long long g0 = s * A.ups, g1 = min(g0 + A.ups, total_units);
+                mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(g1 - g0) * BETA * 1024u);
+                long long g = g0;
+                while (g < g1) {
+                    const int c = static_cast<int>(g / U);
+                    const int k = static_cast<int>(g - static_cast<long long>(c) * U);
+                    const int len = static_cast<int>(min(static_cast<long long>(U - k), g1 - g));
+                    const unsigned char* src = A.calls[c].keys + (u0 + k) * BETA * 1024;
+                    const uint32_t dst = stage_addr(slot) + static_cast<uint32_t>(g - g0) * BETA * 1024u;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+                        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+                        "l"(src), "r"(static_cast<uint32_t>(len) * BETA * 1024u), "r"(smem_u32(&full[slot])),
+                        "l"(pol)
+                        : "memory");
+                    g += len;
+                }
+            }
+        }
+        return;
+    }
+    if (warp == kWLoad) {
+        // -------------------------------- x(c) and alpha(c), ahead of use
+        // TMA bulk copies when the rows are 16-byte aligned and complete;
+        // otherwise the 32 lanes copy (zero-filling rows past x_rows / m).
+        pdl_wait();
+        const long long r0 = static_cast<long long>(gb) * kXBlock;
+        const long long ra = static_cast<long long>(t0) * 32;
+        const long long arows = min(static_cast<long long>(U) * 32, static_cast<long long>(A.m) - ra);
+        for (int c = 0; c < ncalls; ++c) {
+            const int buf = c & 1;
+            const uint32_t par = static_cast<uint32_t>(((c >> 1) - 1) & 1);  // phase of call c-2
+            if (c >= 2) mbar_wait(&xempty[buf], par);
+            const float* x = A.calls[c].x;
+            float* xd = xs + buf * kXBlock;
+            if (r0 + kXBlock <= A.x_rows && (reinterpret_cast<uintptr_t>(x + r0) & 15) == 0) {
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&xfull[buf], kXBlock * 4);
+                    bulk_g2s_plain(xd, x + r0, kXBlock * 4, &xfull[buf]);
+                } else {
+                    mbar_arrive(&xfull[buf]);
+                }
+            } else {
+                float v[kXBlock / 32];
+#pragma unroll
+                for (int q = 0; q < kXBlock / 32; ++q) {
+                    const long long r = r0 + q * 32 + lane;
+                    v[q] = r < A.x_rows ? __ldcg(x + r) : 0.0f;
+                }
+#pragma unroll
+                for (int q = 0; q < kXBlock / 32; ++q) xd[q * 32 + lane] = v[q];
+                mbar_arrive(&xfull[buf]);
+            }
+            if (alpha_smem) {
+                if (c >= 2) mbar_wait(&lempty[buf], par);
+                const float* al = A.calls[c].alpha;
+                float* ad = as + buf * (abuf_bytes / 4);  // [BETA][U*32]
+                const uint32_t nbytes = static_cast<uint32_t>(arows) * 4u;
+                const bool tma = al && (nbytes & 15) == 0 && (A.m & 3) == 0 &&
+                                 (reinterpret_cast<uintptr_t>(al + ra) & 15) == 0;
+                if (tma) {
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&afull[buf], nbytes * BETA);
+#pragma unroll
+                        for (int i = 0; i < BETA; ++i)
+                            bulk_g2s_plain(ad + i * U * 32, al + static_cast<long long>(i) * A.m + ra, nbytes, &afull[buf]);
+                    } else {
+                        mbar_arrive(&afull[buf]);
+                    }
+                } else {
+                    for (int i = 0; i < BETA; ++i) {
+                        for (int k0 = 0; k0 < U * 32; k0 += 32 * 8) {
+                            float v[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const long long rl = k0 + q * 32 + lane;
+                                v[q] = (rl < arows) ? (al ? __ldg(al + static_cast<long long>(i) * A.m + ra + rl) : 1.0f)
+                                                    : 0.0f;
+                            }
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (k0 + q * 32 + lane < U * 32) ad[i * U * 32 + k0 + q * 32 + lane] = v[q];
+                        }
+                    }
+                    mbar_arrive(&afull[buf]);
+                }
+            } else {
+                mbar_arrive(&afull[buf]);
+            }
+        }
+        return;
+    }
+    if (warp >= kWBuild) {
+        // ------------------------------------------- LUT(c) into half c&1
+        const int which = warp - kWBuild;
+        for (int c = 0; c < ncalls; ++c) {
+            const int buf = c & 1;
+            mbar_wait(&xfull[buf], static_cast<uint32_t>((c >> 1) & 1));
+            if (c >= 2) mbar_wait(&lempty[buf], static_cast<uint32_t>(((c >> 1) - 1) & 1));
+            build_tables(which, lut_abs + static_cast<uint32_t>(buf) * 128u + static_cast<uint32_t>(lane) * 4u,
+                         xs + buf * kXBlock, lane);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&xempty[buf]);
+                mbar_arrive(&lfull[buf]);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- consumers
+    uint32_t goff[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) goff[j] = lut_abs | (static_cast<uint32_t>((lane + j) & 31) * 4u);
+    pdl_wait();  // partials of the previous launch may still be read by its finaliser
+    const long long MTP = static_cast<long long>(A.MT) * 32;
+    long long gu = warp;  // this warp's next unit in the CTA's (call, unit) sequence
+    for (int c = 0; c < ncalls; ++c) {
+        const int buf = c & 1;
+        const uint32_t par = static_cast<uint32_t>((c >> 1) & 1);
+        mbar_wait(&lfull[buf], par);
+        mbar_wait(&afull[buf], par);
+        const float* alpha = A.calls[c].alpha;
+        const float* ab = as + buf * (abuf_bytes / 4);
+        float* part = A.partial + (static_cast<long long>(c) * A.NB + gb) * MTP;
+        const long long cend = static_cast<long long>(c + 1) * U;
+        for (; gu < cend; gu += kNC) {
+            const int k = static_cast<int>(gu - static_cast<long long>(c) * U);
+            const long long r = static_cast<long long>(t0 + k) * 32 + lane;
+            float a[BETA];
+#pragma unroll
+            for (int i = 0; i < BETA; ++i) {
+                if (alpha_smem) a[i] = ab[(i * U + k) * 32 + lane];
+                else if (alpha) a[i] = r < A.m ? __ldg(alpha + static_cast<long long>(i) * A.m + r) : 0.0f;
+                else a[i] = 1.0f;
+            }
+            const long long s = gu / A.ups;
+            const int slot = static_cast<int>(s % nst);
+            const int pos = static_cast<int>(gu - s * A.ups);
+            mbar_wait(&full[slot], static_cast<uint32_t>((s / nst) & 1));
+            const uint32_t kbase = stage_addr(slot) + static_cast<uint32_t>(pos) * BETA * 1024u;
+            const double sum = buf == 0 ? stream_unit<BETA, 0>(kbase, lane, goff, a)
+                                        : stream_unit<BETA, 128>(kbase, lane, goff, a);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (r < A.m) part[r] = static_cast<float>(sum);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lempty[buf]);
+    }
+}
+
+__global__ void __launch_bounds__(256) stream_finalize_kernel(const __grid_constant__ StreamArgs A) {
+    pdl_wait();
+    const int c = blockIdx.y;
+    const long long r = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+    if (r >= A.m) return;
+    const long long MTP = static_cast<long long>(A.MT) * 32;
+    const float* p = A.partial + static_cast<long long>(c) * A.NB * MTP + r;
+    double s = 0.0;
+    for (int gb = 0; gb < A.NB; ++gb) s += static_cast<double>(__ldcg(p + gb * MTP));
+    A.calls[c].y[r] = static_cast<float>(s);
+}
+
+template <int BETA>
+cudaError_t launch_stream_beta(const StreamArgs& A, bool pdl, cudaStream_t stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(biqgemm_stream_kernel<BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kStreamSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(A.grid));
+    cfg.blockDim = dim3(kSThreads);
+    cfg.dynamicSmemBytes = kStreamSmem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, biqgemm_stream_kernel<BETA>, A);
+    if (e != cudaSuccess) return e;
+    // finaliser: always PDL-chained behind the stream kernel
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>((A.m + 255) / 256), static_cast<unsigned>(A.ncalls));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&cfg, stream_finalize_kernel, A);
+}
+
+}  // namespace
+
+bool stream_supported(int mu, int beta, long long b) { return mu == kMU && b == 1 && beta >= 1 && beta <= 4; }
+
+size_t stream_workspace_bytes(long long m, long long groups, int count) {
+    const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
+    const long long per = static_cast<long long>(std::min(count, kStreamMaxGroup));
+    return static_cast<size_t>(per * NB * MT * 32) * sizeof(float);
+}
+
+cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
+                                  float* ws, bool pdl, cudaStream_t stream) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    StreamArgs A{};
+    A.x_rows = x_rows;
+    A.m = m;
+    A.NB = (G + 31) / 32;
+    A.MT = (m + 31) / 32;
+    // cpb CTAs per 32-group block, each a contiguous range of >= 1 row
+    // tiles of that block; one CTA per SM when NB <= #SMs
+    A.cpb = std::max(1, std::min(A.MT, sms / A.NB));
+    A.grid = A.cpb * A.NB;
+    A.ups = std::max(1, 12 / beta);  // ~12 KiB ring stages
+    A.partial = ws;
+    for (int done = 0; done < count; done += kStreamMaxGroup) {
+        A.ncalls = std::min(kStreamMaxGroup, count - done);
+        for (int i = 0; i < A.ncalls; ++i) A.calls[i] = calls[done + i];
+        cudaError_t e;
+        switch (beta) {
+            case 1: e = launch_stream_beta<1>(A, pdl || done > 0, stream); break;
+            case 2: e = launch_stream_beta<2>(A, pdl || done > 0, stream); break;
+            case 3: e = launch_stream_beta<3>(A, pdl || done > 0, stream); break;
+            case 4: e = launch_stream_beta<4>(A, pdl || done > 0, stream); break;
+            default: return cudaErrorInvalidValue;
+        }
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace bqg

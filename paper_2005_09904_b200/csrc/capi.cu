@@ -486,6 +486,58 @@ extern "C" int bqg_biqgemm_f32(const uint8_t* d_keys, const float* d_alpha, cons
     return BQG_OK;
 }
 
+extern "C" size_t bqg_biqgemm_grouped_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                                      size_t count) {
+    if (mu < 1 || mu > 8 || m == 0 || n == 0 || b == 0 || beta == 0 || count == 0) return 0;
+    const size_t single = bqg_biqgemm_workspace_bytes(m, n, b, beta, mu);
+    if (!bqg::stream_supported(static_cast<int>(mu), static_cast<int>(beta), static_cast<long long>(b)))
+        return single;
+    const size_t grouped = bqg::stream_workspace_bytes(static_cast<long long>(m),
+                                                       static_cast<long long>(groups_of(n, mu)),
+                                                       static_cast<int>(std::min<size_t>(count, 1u << 30)));
+    return std::max(single, grouped);
+}
+
+extern "C" int bqg_biqgemm_grouped_f32(const bqg_call* h_calls, size_t count, size_t x_rows, size_t m, size_t n,
+                                       size_t b, unsigned beta, unsigned mu, void* d_ws, size_t ws_bytes, int pdl,
+                                       void* stream) {
+    int s = check_mu(mu, "biqgemm");
+    if (s) return s;
+    if (mu > 8) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_grouped: fast path needs mu <= 8 (use the exact path)");
+    s = check_dims(m, n, "biqgemm");
+    if (s) return s;
+    if (beta == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: beta must be >= 1");
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    if (count == 0) return BQG_OK;
+    if (!h_calls || !d_ws) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_grouped: null pointer");
+    for (size_t i = 0; i < count; ++i)
+        if (!h_calls[i].d_keys_tiled || !h_calls[i].d_x || !h_calls[i].d_y)
+            return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_grouped: null pointer in call %zu", i);
+    if (ws_bytes < bqg_biqgemm_grouped_workspace_bytes(m, n, b, beta, mu, count))
+        return set_err(BQG_ERR_WORKSPACE, "biqgemm_grouped: workspace %zu < %zu bytes", ws_bytes,
+                       bqg_biqgemm_grouped_workspace_bytes(m, n, b, beta, mu, count));
+    if (m > 0x7fffffff || count > 0x7fffffff) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: dimension too large");
+    BQG_NEED_DEVICE();
+    if (!bqg::stream_supported(static_cast<int>(mu), static_cast<int>(beta), static_cast<long long>(b))) {
+        for (size_t i = 0; i < count; ++i) {
+            s = bqg_biqgemm_f32(h_calls[i].d_keys_tiled, h_calls[i].d_alpha, h_calls[i].d_x, x_rows, h_calls[i].d_y,
+                                m, n, b, beta, mu, d_ws, ws_bytes, pdl || i > 0, stream);
+            if (s) return s;
+        }
+        return BQG_OK;
+    }
+    std::vector<bqg::StreamCall> calls(count);
+    for (size_t i = 0; i < count; ++i)
+        calls[i] = {h_calls[i].d_keys_tiled, h_calls[i].d_alpha, h_calls[i].d_x, h_calls[i].d_y};
+    cudaError_t e = bqg::launch_biqgemm_stream(calls.data(), static_cast<int>(count), static_cast<long long>(x_rows),
+                                               static_cast<int>(m), static_cast<int>(groups_of(n, mu)),
+                                               static_cast<int>(beta), static_cast<float*>(d_ws), pdl != 0,
+                                               as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "biqgemm grouped kernels");
+    return BQG_OK;
+}
+
 extern "C" size_t bqg_biqgemm_exact_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu) {
     if (mu < 1 || mu > 16 || m == 0 || n == 0 || b == 0 || beta == 0) return 0;
     return bqg::exact_workspace_bytes(static_cast<long long>(m), static_cast<long long>(n), static_cast<int>(beta),

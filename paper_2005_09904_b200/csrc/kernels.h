@@ -37,6 +37,20 @@ struct QueryParams {
     int debug;  // profiling switches (BQG_DEBUG_FLAGS); 0 in production
 };
 
+// Grouped ("stream") form: a group of independent calls sharing (m, n, beta,
+// mu); b == 1, mu == 8, beta <= 4 (biqgemm_stream.cu).
+struct StreamCall {
+    const uint8_t* keys;  // tiled
+    const float* alpha;   // beta x m or nullptr
+    const float* x;       // x_rows x 1
+    float* y;             // m x 1
+};
+constexpr int kStreamMaxGroup = 128;  // calls per launch (kernel-parameter array)
+bool stream_supported(int mu, int beta, long long b);
+size_t stream_workspace_bytes(long long m, long long groups, int count);
+cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
+                                  float* ws, bool pdl, cudaStream_t stream);
+
 // Workspace for the fast path (bytes).
 size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b);
 // Grid planner: CTAs per 32-group block.

@@ -1,0 +1,114 @@
+"""Grouped calls (bqg_biqgemm_grouped_f32): every entry is a full biqgemm
+call (kernel.hpp:246-258) with its own weights, alpha and x.  Each y must
+meet the fp32 contract against the oracle (the reference's algorithm, fp64
+accumulation), be deterministic, and not depend on the group size or the
+grid (bitwise)."""
+import numpy as np
+import pytest
+
+from test_gpu_parity import assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def make_group(bq, torch, count, m, n, beta, mu, seed, plane_mode=False, x_rows=None, b=1):
+    x_rows = n if x_rows is None else x_rows
+    entries, host = [], []
+    for i in range(count):
+        w = bq.random_uniform(m, n, seed + 17 * i)
+        layer = bq.PackedLinear.from_weights(w, beta, mu)
+        keys, alpha = layer.export()
+        layer.close()
+        x = bq.random_normal(x_rows, b, seed + 17 * i + 1)
+        tiled = bq.tile_keys(torch.from_numpy(keys).cuda(), n, mu)
+        a = None if plane_mode else torch.from_numpy(alpha).cuda()
+        y = torch.full((m, b), float("nan"), device="cuda")
+        entries.append((tiled, a, torch.from_numpy(x).cuda(), y))
+        host.append((keys, None if plane_mode else alpha, x))
+    return entries, host
+
+
+def run_group(bq, entries, x_rows, m, n, b, beta, mu, pdl=False):
+    import torch
+
+    ws = bq.grouped_workspace(m, n, b, beta, mu, len(entries))
+    bq.biqgemm_grouped_device(entries, x_rows, m, n, b, beta, mu, ws, pdl=pdl)
+    torch.cuda.synchronize()
+    return [e[3].cpu().numpy().copy() for e in entries]
+
+
+@pytest.mark.parametrize("count,m,n,beta", [
+    (1, 1, 1, 1), (3, 33, 7, 2), (5, 100, 300, 3), (4, 64, 2048, 4), (2, 1000, 777, 3), (6, 4096, 4096, 3),
+    (3, 2000, 4100, 1), (2, 16384, 4096, 3), (2, 257, 8200, 2),
+])
+def test_grouped_vs_port(bq, port, cuda, count, m, n, beta):
+    import torch
+
+    entries, host = make_group(bq, torch, count, m, n, beta, 8, 100 + m + n)
+    ys = run_group(bq, entries, n, m, n, 1, beta, 8)
+    for (keys, alpha, x), y in zip(host, ys):
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x)
+        assert_close(y, y_ref)
+    # deterministic, and independent of the group size (each call alone)
+    assert all(np.array_equal(a, b) for a, b in zip(run_group(bq, entries, n, m, n, 1, beta, 8), ys))
+    for e, y in zip(entries[:2], ys[:2]):
+        assert np.array_equal(run_group(bq, [e], n, m, n, 1, beta, 8)[0], y)
+
+
+def test_grouped_plane_mode_short_x_and_chunking(bq, port, cuda):
+    """alpha == NULL (biqgemm_plane, kernel.hpp:209-215), x shorter than n
+    (zero-padded rows, kernel.hpp:132), and more calls than one launch holds
+    (kStreamMaxGroup = 128) with PDL between the launches."""
+    import torch
+
+    m, n, beta = 70, 600, 2
+    entries, host = make_group(bq, torch, 131, m, n, beta, 8, 7, plane_mode=True, x_rows=555)
+    ys = run_group(bq, entries, 555, m, n, 1, beta, 8, pdl=True)
+    for (keys, _, x), y in zip(host, ys):
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), None, n, 8, x)
+        assert_close(y, y_ref)
+
+
+@pytest.mark.parametrize("b,mu", [(2, 8), (1, 6), (5, 8)])
+def test_grouped_other_shapes_use_single_call_kernels(bq, port, cuda, b, mu):
+    import torch
+
+    m, n, beta = 150, 500, 3
+    entries, host = make_group(bq, torch, 3, m, n, beta, mu, 21, b=b)
+    ys = run_group(bq, entries, n, m, n, b, beta, mu)
+    for (keys, alpha, x), y in zip(host, ys):
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x)
+        assert_close(y, y_ref)
+
+
+def test_grouped_row_sharding_bitwise(bq, cuda):
+    """32-row-aligned row shards of a grouped call reproduce y bitwise (the
+    multi-GPU decomposition of the stream form)."""
+    import torch
+
+    m, n, beta = 1000, 2500, 3
+    entries, host = make_group(bq, torch, 2, m, n, beta, 8, 99)
+    ys = run_group(bq, entries, n, m, n, 1, beta, 8)
+    for (keys, alpha, x), y in zip(host, ys):
+        for k in (2, 3, 8):
+            bounds = [min(m, 32 * ((m * i // k + 31) // 32)) for i in range(k + 1)]
+            parts = []
+            for a, z in zip(bounds[:-1], bounds[1:]):
+                t = bq.tile_keys(torch.from_numpy(np.ascontiguousarray(keys[:, a:z])).cuda(), n, 8)
+                al = torch.from_numpy(np.ascontiguousarray(alpha[:, a:z])).cuda()
+                yy = torch.empty((z - a, 1), device="cuda")
+                parts.append(run_group(bq, [(t, al, torch.from_numpy(x).cuda(), yy)], n, z - a, n, 1, beta, 8)[0])
+            assert np.array_equal(np.concatenate(parts), y)
+
+
+def test_grouped_rejects_bad_arguments(bq, cuda):
+    import torch
+    from paper_2005_09904_b200 import _capi
+
+    entries, _ = make_group(bq, torch, 2, 64, 256, 2, 8, 5)
+    ws = bq.grouped_workspace(64, 256, 1, 2, 8, 2)
+    small = bq.Workspace(16)
+    with pytest.raises(_capi.BiqgemmError):
+        bq.biqgemm_grouped_device(entries, 256, 64, 256, 1, 2, 8, small)
+    with pytest.raises(_capi.InvalidArgument):
+        bq.biqgemm_grouped_device(entries, 257, 64, 256, 1, 2, 8, ws)  # x longer than G*mu
