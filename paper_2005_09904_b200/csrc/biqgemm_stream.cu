@@ -127,13 +127,13 @@ __device__ __forceinline__ void build_tables(int which, uint32_t col, const floa
 // gather_chunk in query_core.cuh).  IMM selects the buffer half (+128 B).
 template <int IMM>
 __device__ __forceinline__ float stream_gather(const uint32_t (&w)[8], const uint32_t (&goff)[32]) {
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float acc[4];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const uint32_t off = __byte_perm(goff[j], w[j >> 2], 0x3200u | ((4u + (j & 3)) << 4));
         float e;
         asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off), "n"(IMM));
-        acc[j & 3] += e;
+        acc[j & 3] = j < 4 ? e : acc[j & 3] + e;  // 0 + e == e (up to the sign of a zero sum)
     }
     return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             for (long long s = lane; s < nstages_total; s += nst) {
                 const int slot = lane;
                 const long long round = s / nst;
-                if (round > 0) mbar_wait(&empty[slot], static_cast<uint32_t>((round - 1) & 1));
+                if (round > 0) mbar_wait_sleep(&empty[slot], static_cast<uint32_t>((round - 1) & 1));
                 const long long g0 = s * A.ups, g1 = min(g0 + A.ups, total_units);
                 mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(g1 - g0) * BETA * 1024u);
                 long long g = g0;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         for (int c = 0; c < ncalls; ++c) {
             const int buf = c & 1;
             const uint32_t par = static_cast<uint32_t>(((c >> 1) - 1) & 1);  // phase of call c-2
-            if (c >= 2) mbar_wait(&xempty[buf], par);
+            if (c >= 2) mbar_wait_sleep(&xempty[buf], par);
             const float* x = A.calls[c].x;
             float* xd = xs + buf * kXBlock;
             if (r0 + kXBlock <= A.x_rows && (reinterpret_cast<uintptr_t>(x + r0) & 15) == 0) {
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
                 mbar_arrive(&xfull[buf]);
             }
             if (alpha_smem) {
-                if (c >= 2) mbar_wait(&lempty[buf], par);
+                if (c >= 2) mbar_wait_sleep(&lempty[buf], par);
                 const float* al = A.calls[c].alpha;
                 float* ad = as + buf * (abuf_bytes / 4);  // [BETA][U*32]
                 const uint32_t nbytes = static_cast<uint32_t>(arows) * 4u;
@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         const int which = warp - kWBuild;
         for (int c = 0; c < ncalls; ++c) {
             const int buf = c & 1;
-            mbar_wait(&xfull[buf], static_cast<uint32_t>((c >> 1) & 1));
-            if (c >= 2) mbar_wait(&lempty[buf], static_cast<uint32_t>(((c >> 1) - 1) & 1));
+            mbar_wait_sleep(&xfull[buf], static_cast<uint32_t>((c >> 1) & 1));
+            if (c >= 2) mbar_wait_sleep(&lempty[buf], static_cast<uint32_t>(((c >> 1) - 1) & 1));
             build_tables(which, lut_abs + static_cast<uint32_t>(buf) * 128u + static_cast<uint32_t>(lane) * 4u,
                          xs + buf * kXBlock, lane);
             __syncwarp();
@@ -341,7 +341,13 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     for (int j = 0; j < 32; ++j) goff[j] = lut_abs | (static_cast<uint32_t>((lane + j) & 31) * 4u);
     pdl_wait();  // partials of the previous launch may still be read by its finaliser
     const long long MTP = static_cast<long long>(A.MT) * 32;
-    long long gu = warp;  // this warp's next unit in the CTA's (call, unit) sequence
+    // This warp's units are gu = warp, warp + kNC, ... of the CTA's (call,
+    // unit) sequence; their ring position (stage slot, unit in stage,
+    // phase) advances incrementally -- no divisions in the loop.
+    int gu = warp;
+    int pos = gu % A.ups, slot = (gu / A.ups) % nst;
+    uint32_t kphase = static_cast<uint32_t>((gu / A.ups) / nst) & 1u;
+    const int adv_q = kNC / A.ups, adv_r = kNC - (kNC / A.ups) * A.ups;
     for (int c = 0; c < ncalls; ++c) {
         const int buf = c & 1;
         const uint32_t par = static_cast<uint32_t>((c >> 1) & 1);
@@ -350,9 +356,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         const float* alpha = A.calls[c].alpha;
         const float* ab = as + buf * (abuf_bytes / 4);
         float* part = A.partial + (static_cast<long long>(c) * A.NB + gb) * MTP;
-        const long long cend = static_cast<long long>(c + 1) * U;
-        for (; gu < cend; gu += kNC) {
-            const int k = static_cast<int>(gu - static_cast<long long>(c) * U);
+        const int cbase = c * U;
+        for (; gu < cbase + U; gu += kNC) {
+            const int k = gu - cbase;
             const long long r = static_cast<long long>(t0 + k) * 32 + lane;
             float a[BETA];
 #pragma unroll
@@ -361,16 +367,25 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
                 else if (alpha) a[i] = r < A.m ? __ldg(alpha + static_cast<long long>(i) * A.m + r) : 0.0f;
                 else a[i] = 1.0f;
             }
-            const long long s = gu / A.ups;
-            const int slot = static_cast<int>(s % nst);
-            const int pos = static_cast<int>(gu - s * A.ups);
-            mbar_wait(&full[slot], static_cast<uint32_t>((s / nst) & 1));
+            mbar_wait(&full[slot], kphase);
             const uint32_t kbase = stage_addr(slot) + static_cast<uint32_t>(pos) * BETA * 1024u;
             const double sum = buf == 0 ? stream_unit<BETA, 0>(kbase, lane, goff, a)
                                         : stream_unit<BETA, 128>(kbase, lane, goff, a);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (r < A.m) part[r] = static_cast<float>(sum);
+            // advance the ring position by kNC units
+            pos += adv_r;
+            int adv = adv_q;
+            if (pos >= A.ups) {
+                pos -= A.ups;
+                ++adv;
+            }
+            slot += adv;
+            if (slot >= nst) {
+                slot -= nst;
+                kphase ^= 1u;
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&lempty[buf]);

@@ -122,6 +122,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         ::"r"(smem_u32(bar)), "r"(parity)
         : "memory");
 }
+// Same, but the thread may sleep until the phase completes (suspend-time
+// hint): for warps that wait long (producers, builders, loaders) so that
+// their retries do not take issue slots from the gather warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}"
+        ::"r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+}
 // Global -> shared bulk copy completed on `bar` (complete_tx), L2 policy hint.
 // bytes % 16 == 0, both addresses 16-byte aligned.
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar,
