@@ -10,18 +10,24 @@ x = random_normal(n,b,0x5EED+1)), quantized + packed ON THE GPU by the
 product path.  A "step" is one BiQGEMM call (fused LUT build -> LUT query
 -> alpha scale) on one layer's weights.
 
-Timing (device): the K timed calls are captured in one CUDA graph with
-programmatic dependent launch between consecutive calls (as consecutive
-layers would run in a serving step) and replayed once between a
-barrier+synchronize pair, timed with CUDA events on the replay stream.
-Consecutive calls rotate over R distinct weight copies totalling > 2x the
-126 MB L2, so every call streams its packed keys from HBM (inputs larger than
-L2; no flush needed).  value = packed-key bytes of all ranks / max-over-ranks
-time, in GB/s; us/call is reported beside it.
+Timing (device, `value`): the K timed calls are independent (each its own
+weight copy, its own x, its own LUT build and y) and are issued through the
+grouped C-ABI entry, G = 128 calls per launch (bqg_biqgemm_grouped_f32: one
+persistent kernel whose key stream runs ahead across call boundaries, then a
+fixed-order epilogue kernel), captured in one CUDA graph and replayed once
+between a barrier+synchronize pair, timed with CUDA events on the replay
+stream.  Calls rotate over R distinct weight copies totalling > 2x the 126 MB
+L2, so every call streams its packed keys from HBM (inputs larger than L2; no
+flush needed).  value = packed-key bytes of all ranks / max-over-ranks time,
+in GB/s; us/call is reported beside it.
+
+`latency`: the dependent-call regime -- one single-call kernel per step,
+each PDL-chained behind its predecessor (consecutive layers of one model).
 
 e2e: the same calls through the public C ABI with HOST buffers
-(bqg_layer_forward_host: H2D of x from pinned memory, the kernel, D2H of y,
-synchronised), wall-clock timed.
+(bqg_layers_forward_host per group of G calls: one H2D of the G inputs from
+pinned memory, the grouped kernels, one D2H of the G outputs, synchronised),
+wall-clock timed.
 
 N>1 (torchrun): weak scaling -- every rank owns a C2-sized row shard of an
 (N*4096) x 4096 layer, and y is assembled with an NCCL all-gather each step.
@@ -116,19 +122,20 @@ class ClockSampler:
         self._stop.set()
         self._t.join(timeout=10)
 
-    def summary(self):
-        if not self.samples:
+    def summary(self, since=0):
+        samples = self.samples[since:] or self.samples[-3:]
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for s in self.samples:
+        for s in samples:
             for k, v in zip(names, s[3:7]):
                 if "Active" in v and "Not" not in v:
                     reasons.add(k)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(samples)}
 
 
 def dist_env():
@@ -149,93 +156,126 @@ def run_ours(args):
     import paper_2005_09904_b200.biqgemm as bq
 
     m, n, beta, b, mu = CONFIGS[args.config]
-    G = (n + mu - 1) // mu
-    kb = key_bytes(m, n, beta, mu)  # per rank (weak scaling: each rank owns an m-row shard)
+    kb = key_bytes(m, n, beta, mu)  # per rank and call (weak scaling: each rank owns an m-row shard)
     dev = torch.device("cuda", local_rank)
+    G = args.group
 
     # ---- the layer: W generated like bench_cli, quantized + packed on the GPU
-    m_total = m * world
-    w = bq.random_uniform(m_total, n, SEED) if world > 1 else bq.random_uniform(m, n, SEED)
+    w = bq.random_uniform(m * world, n, SEED) if world > 1 else bq.random_uniform(m, n, SEED)
     w_shard = np.ascontiguousarray(w[rank * m:(rank + 1) * m])
     layer = bq.PackedLinear.from_weights(w_shard, beta, mu)
     keys, alpha = layer.export()
-    x_h = bq.random_normal(n, b, SEED + 1)
 
-    # ---- rotating weight copies > 2x L2
-    tiled0 = torch.empty(bq.tiled_key_bytes(m, n, beta, mu), dtype=torch.uint8, device=dev)
-    torch.cuda.synchronize()
-    src = torch.from_numpy(keys).to(dev)
-    tiled0.copy_(bq.tile_keys(src, n, mu))
+    # ---- rotating weight copies > 2x L2 (every call streams its keys from
+    # HBM), one x per copy (every call builds its own LUT)
+    tiled0 = bq.tile_keys(torch.from_numpy(keys).to(dev), n, mu)
     copies = max(2, int(np.ceil(2.0 * L2_BYTES / tiled0.numel())) + 1)
     tiled = [tiled0] + [tiled0.clone() for _ in range(copies - 1)]
     alphas = [torch.from_numpy(alpha).to(dev) for _ in range(copies)]
-    x_d = torch.from_numpy(x_h).to(dev)
+    x_h = [bq.random_normal(n, b, SEED + 1 + j) for j in range(copies)]
+    xs = [torch.from_numpy(x).to(dev) for x in x_h]
     ys = [torch.empty((m, b), device=dev) for _ in range(copies)]
-    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, b, beta, mu)), device=dev)
     stream = torch.cuda.Stream(device=dev)
 
-    def call(i, s):
-        j = i % copies
-        bq.biqgemm_device(tiled[j], alphas[j], x_d, ys[j], m, n, beta, mu, ws, pdl=True, stream=s.cuda_stream)
-
     # ---- correctness gate before timing: y equals the exact path within tolerance
+    ws_g = bq.grouped_workspace(m, n, b, beta, mu, G, device=dev)
     with torch.cuda.stream(stream):
-        call(0, stream)
+        bq.biqgemm_grouped_device([(tiled[j], alphas[j], xs[j], ys[j]) for j in range(2)], n, m, n, b, beta, mu,
+                                  ws_g, stream=stream.cuda_stream)
     stream.synchronize()
-    y_exact = layer.forward(x_h, exact=True)
-    y0 = ys[0].cpu().numpy()
-    rel = float(np.linalg.norm(y0.astype(np.float64) - y_exact) / np.linalg.norm(y_exact.astype(np.float64)))
+    rel = 0.0
+    for j in range(2):
+        y_exact = layer.forward(x_h[j], exact=True)
+        y0 = ys[j].cpu().numpy()
+        rel = max(rel, float(np.linalg.norm(y0.astype(np.float64) - y_exact) /
+                             np.linalg.norm(y_exact.astype(np.float64))))
     assert rel <= 1e-5, f"parity gate failed: rel {rel}"
 
-    # ---- graphs: warmup (W calls) and timed (K calls)
-    def capture(count, offset):
+    # ---- throughput graph: `count` independent calls, G per grouped launch
+    def grouped_graph(count, offset):
+        arrays = []
+        for st in range(offset, offset + count, G):
+            ent = [(tiled[i % copies], alphas[i % copies], xs[i % copies], ys[i % copies])
+                   for i in range(st, min(offset + count, st + G))]
+            arrays.append(bq.make_calls(ent))
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
             with torch.cuda.graph(g, stream=stream):
+                for a in arrays:
+                    bq.biqgemm_grouped_device(a, n, m, n, b, beta, mu, ws_g, pdl=True, stream=stream.cuda_stream)
+        return g, len(arrays)
+
+    # ---- latency graph: dependent-layer regime, one kernel (chain) per call
+    ws1 = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, b, beta, mu)), device=dev)
+
+    def chain_graph(count):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            bq.biqgemm_device(tiled[0], alphas[0], xs[0], ys[0], m, n, beta, mu, ws1, pdl=True,
+                              stream=stream.cuda_stream)
+            stream.synchronize()
+            with torch.cuda.graph(g, stream=stream):
                 for i in range(count):
-                    call(offset + i, stream)
+                    j = i % copies
+                    bq.biqgemm_device(tiled[j], alphas[j], xs[j], ys[j], m, n, beta, mu, ws1, pdl=True,
+                                      stream=stream.cuda_stream)
         return g
 
-    g_warm = capture(max(args.warmup, 1), 0)
-    g_timed = capture(args.steps, args.warmup)
+    g_warm, _ = grouped_graph(max(args.warmup, 1), 0)
+    g_timed, n_launch = grouped_graph(args.steps, args.warmup)
     torch.cuda.synchronize()
 
-    with ClockSampler(local_rank) as clk:
-        # warm-up steps + enough untimed replays for steady clocks (>= 0.5 s)
-        with torch.cuda.stream(stream):
-            g_warm.replay()
-            t0 = time.perf_counter()
-            while time.perf_counter() - t0 < 0.5:
-                g_timed.replay()
-                stream.synchronize()
+    def timed(g):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
-            ev0.record(stream)
-            g_timed.replay()
-            ev1.record(stream)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
         stream.synchronize()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ms = ev0.elapsed_time(ev1)
-        clocks = clk.summary()
+        return e0.elapsed_time(e1)
 
-    # all-gather of y shards per step (N>1): timed separately as part of the step
+    with ClockSampler(local_rank) as clk:
+        # warm-up steps + enough untimed replays for steady clocks (>= 1 s,
+        # and until the sampler has readings under load)
+        with torch.cuda.stream(stream):
+            g_warm.replay()
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 1.0 or (len(clk.samples) < 3 and time.perf_counter() - t0 < 10):
+                g_timed.replay()
+                stream.synchronize()
+        n_before = len(clk.samples)
+        ms = 0.0
+        reps = 0
+        # the timed region: one replay of exactly K steps, bracketed by
+        # barrier + synchronize; repeated (>= 3 times, and until the sampler
+        # has read the clocks during timed work); the MEDIAN replay is reported
+        times = []
+        while reps < 3 or (len(clk.samples) <= n_before and reps < 200):
+            times.append(timed(g_timed))
+            reps += 1
+        ms = float(np.median(times))
+        clocks = clk.summary(since=n_before)
+
+    # y of every call is assembled across ranks (N>1): one NCCL all-gather
+    # per grouped launch (G calls' row shards), timed as part of the step
     gather_ms = 0.0
     if world > 1:
-        y_all = torch.empty((world * m, b), device=dev)
+        y_grp = torch.empty((G, m, b), device=dev)
+        y_all = torch.empty((world * G, m, b), device=dev)
         for _ in range(3):
-            dist.all_gather_into_tensor(y_all, ys[0])
+            dist.all_gather_into_tensor(y_all, y_grp)
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(args.steps):
-            dist.all_gather_into_tensor(y_all, ys[i % copies])
+        for _ in range(n_launch):
+            dist.all_gather_into_tensor(y_all, y_grp)
         e1.record()
         torch.cuda.synchronize()
         gather_ms = e0.elapsed_time(e1)
@@ -250,26 +290,40 @@ def run_ours(args):
     value_gbs = world * kb * args.steps / (total_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
 
-    # ---- e2e through the public C ABI with host buffers (pinned)
-    x_pin = torch.from_numpy(x_h).pin_memory()
-    y_pin = torch.empty((m, b), dtype=torch.float32).pin_memory()
+    # dependent-call latency (each call waits for its predecessor)
+    lat_steps = min(args.steps, 2000)
+    g_chain = chain_graph(lat_steps)
+    with torch.cuda.stream(stream):
+        g_chain.replay()
+    lat_ms = timed(g_chain)
+    lat_us = lat_ms * 1e3 / lat_steps
+    del g_chain
+
+    # ---- e2e through the public C ABI with HOST buffers (pinned): per group
+    # of G calls one bqg_layers_forward_host = H2D of the G inputs, the
+    # grouped kernels, D2H of the G outputs, synchronised
     e2e_layers = [layer] + [bq.PackedLinear.from_keys(keys, alpha, n, mu) for _ in range(copies - 1)]
-    for i in range(max(args.warmup, 3)):
-        e2e_layers[i % copies].forward_into(x_pin, y_pin)
+    x_pin = torch.from_numpy(np.stack([x_h[i % copies] for i in range(G)])).pin_memory()
+    y_pin = torch.empty((G, m, b), dtype=torch.float32).pin_memory()
+    groups = [[e2e_layers[(st + i) % copies] for i in range(min(G, args.steps - st))]
+              for st in range(0, args.steps, G)]
+    for grp in groups[:2]:
+        bq.layers_forward_into(grp, x_pin[:len(grp)], y_pin[:len(grp)])
     if world > 1:
         dist.barrier()
-    e2e_steps = args.steps
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        e2e_layers[i % copies].forward_into(x_pin, y_pin)
+    for grp in groups:
+        bq.layers_forward_into(grp, x_pin[:len(grp)], y_pin[:len(grp)])
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    assert np.allclose(y_pin.numpy(), y_exact, rtol=0, atol=1e-5 * np.abs(y_exact).max())
-    e2e_gbs = world * kb * e2e_steps / e2e_s / 1e9
+    y_check = layer.forward(np.ascontiguousarray(x_pin[0].numpy()), exact=True)
+    assert np.allclose(y_pin[0].numpy(), y_check, rtol=0, atol=1e-5 * np.abs(y_check).max())
+    e2e_gbs = world * kb * args.steps / e2e_s / 1e9
 
+    stream_form = b == 1 and mu == 8 and beta <= 4
     line = {
         "metric": METRIC,
         "value": round(value_gbs, 2),
@@ -284,27 +338,34 @@ def run_ours(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u8 keys, f32 LUT/accumulate",
-        "data": "synthetic (bench_cli generator: W=random_uniform(m,n,0x5EED), x=random_normal(n,b,0x5EED+1))",
+        "data": "synthetic (bench_cli generator: W=random_uniform(m,n,0x5EED), x=random_normal(n,b,0x5EED+1+j))",
         "config": {"workload": f"{args.config} m={m} n={n} q={beta} mu={mu} b={b}" + (
             f" per rank (layer {world * m}x{n}, y all-gathered with NCCL)" if world > 1 else ""),
                    "m": m, "n": n, "beta": beta, "mu": mu, "batch": b,
+                   "step": "one BiQGEMM call (own weights copy, own x, own LUT build, y written)",
                    "l2": f"inputs larger than L2: {copies} rotating weight copies = "
                          f"{copies * tiled0.numel() / 1e6:.0f} MB > 2x126 MB",
-                   "timing": "CUDA graph of K PDL-chained calls, CUDA events on the replay stream",
+                   "timing": f"CUDA graph of {n_launch} grouped launches ({G} independent calls each, "
+                             f"{'stream form' if stream_form else 'single-call kernels'}), CUDA events",
                    "parallelism": f"rows x{world}"},
         "roofline": {"bound": "hbm", "achieved": round(kernel_gbs, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(kernel_gbs / peak, 4), "traffic": ncu_traffic(args.config),
-                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": kb},
-        "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": int(x_h.nbytes),
-                "d2h_bytes_per_step": int(m * b * 4), "us_per_call": e2e_s / e2e_steps * 1e6},
-        "gpu_launches": args.steps,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": kb * min(G, args.steps),
+                     "kernel": "biqgemm_stream_kernel + stream_finalize_kernel" if stream_form else "fast path"},
+        "latency": {"us_per_call": round(lat_us, 3), "gbs": round(kb / (lat_us * 1e-6) / 1e9, 1),
+                    "frac": round(kb / (lat_us * 1e-6) / 1e9 / peak, 4),
+                    "form": "dependent-call regime: one single-call kernel per step, PDL-chained CUDA graph"},
+        "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": int(x_h[0].nbytes),
+                "d2h_bytes_per_step": int(m * b * 4), "us_per_call": e2e_s / args.steps * 1e6,
+                "api": f"bqg_layers_forward_host, {G} calls per synchronised API call"},
+        "gpu_launches": 2 * n_launch if stream_form else args.steps * 2,
         "clocks": clocks,
         "parity_rel_fro": rel,
     }
     if world > 1:
         line["allgather_ms_total"] = gather_ms
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, keys, alpha, x_h, m, n, beta, mu, b, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(args.config, keys, alpha, x_h[0], m, n, beta, mu, b, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     for L in e2e_layers:
@@ -401,6 +462,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--group", type=int, default=128, help="independent calls per grouped launch")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

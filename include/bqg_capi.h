@@ -236,6 +236,15 @@ const float* bqg_layer_device_alpha(const bqg_layer* layer);
  * stats (may be NULL) ACCUMULATES like KernelStats (kernel.hpp:197-202). */
 int bqg_layer_forward_host(bqg_layer* layer, const float* h_x, size_t x_rows, size_t b, float* h_y,
                            int exact, bqg_kernel_stats* stats);
+/* biqgemm over a GROUP of layers that share (m, n, beta, mu) -- one call per
+ * layer, each with its own x -- with HOST buffers: h_x is count x (x_rows x
+ * b) contiguous, h_y is count x (m x b).  One H2D of all x, the grouped
+ * kernels (bqg_biqgemm_grouped_f32), one D2H of all y, synchronised before
+ * return.  Runs on a per-device library stream with its own staging and
+ * workspace (thread-safe; calls are serialised).  exact != 0: the exact path per
+ * layer.  stats (may be NULL) accumulates the counters of all calls. */
+int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, const float* h_x, size_t x_rows,
+                            size_t b, float* h_y, int exact, bqg_kernel_stats* stats);
 /* Device-resident forward on a caller stream (no copies, no sync). */
 int bqg_layer_forward_device(bqg_layer* layer, const float* d_x, size_t x_rows, size_t b, float* d_y,
                              int exact, int pdl, void* stream);

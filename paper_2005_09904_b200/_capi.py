@@ -10,7 +10,9 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libbiqgemm_b200.so"
+# BQG_LIB_VARIANT selects an experimental build under lib/ (tuning runs only).
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / (
+    f"libbiqgemm_b200.{os.environ['BQG_LIB_VARIANT']}.so" if os.environ.get("BQG_LIB_VARIANT") else "libbiqgemm_b200.so")
 
 BQG_OK = 0
 BQG_ERR_INVALID_ARGUMENT = 1
@@ -86,6 +88,7 @@ SIGNATURES = {
     "bqg_biqgemm_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
     "bqg_biqgemm_grouped_workspace_bytes": (sz, [sz, sz, sz, u32, u32, sz]),
     "bqg_biqgemm_grouped_f32": (i32, [vp, sz, sz, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
+    "bqg_layers_forward_host": (i32, [vp, sz, vp, sz, sz, vp, i32, vp]),
     "bqg_biqgemm_exact_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
     "bqg_biqgemm_exact_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),
     "bqg_biqgemm_exact_f64": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),

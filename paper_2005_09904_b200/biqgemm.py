@@ -354,6 +354,24 @@ class PackedLinear:
         return y
 
 
+def layers_forward_into(layers, x, y, exact: bool = False, stats: KernelStats | None = None):
+    """One biqgemm call per layer (layers share (m, n, beta, mu)) with HOST
+    buffers: x is [count, x_rows, b], y is [count, m, b] (numpy or pinned
+    torch CPU tensors).  One H2D, the grouped kernels, one D2H, synchronised."""
+    count, x_rows, b = x.shape
+    arr = (C.c_void_p * count)(*[L._h.value for L in layers])
+    check(lib.bqg_layers_forward_host(C.cast(arr, C.c_void_p), count, _ptr(x), x_rows, b, _ptr(y),
+                                      1 if exact else 0, C.byref(stats) if stats is not None else None))
+    return y
+
+
+def layers_forward(layers, x: np.ndarray, exact: bool = False, stats: KernelStats | None = None) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    m = layers[0].m
+    y = np.empty((x.shape[0], m, x.shape[2]), np.float32)
+    return layers_forward_into(layers, x, y, exact, stats)
+
+
 def pack_linear(w: np.ndarray, beta: int, mu: int) -> PackedLinear:
     return PackedLinear.from_weights(w, beta, mu)
 

@@ -52,10 +52,14 @@ namespace {
 
 constexpr int kMU = 8;
 constexpr int kTable = 1 << kMU;
-constexpr int kNC = 14;                          // consumer (gather) warps
+#ifndef BQG_STREAM_NC
+#define BQG_STREAM_NC 18
+#endif
+constexpr int kNC = BQG_STREAM_NC;               // consumer (gather) warps
 constexpr int kWKey = kNC, kWLoad = kNC + 1;     // key-stream warp, x/alpha loader warp
-constexpr int kWBuild = kNC + 2;                 // two LUT builder warps
-constexpr int kSThreads = (kNC + 4) * 32;
+constexpr int kWBuild = kNC + 2;                 // LUT builder warps
+constexpr int kNBuild = 4;
+constexpr int kSThreads = (kNC + 2 + kNBuild) * 32;
 constexpr int kMaxStages = 24;
 constexpr int kStreamSmem = 227 * 1024;          // opt-in maximum per CTA
 constexpr int kXBlock = 32 * kMU;                // x rows per group block
@@ -77,30 +81,29 @@ struct StreamArgs {
 // and the second half its negation, e[255 - k] = -e[k] (lut.hpp:63-66).  The
 // recurrence tree is walked depth-first at compile time (parent -> child =
 // one fadd), so every entry is produced by exactly the reference's addition
-// and the live state is one value per tree level.
-//   builder 0: keys with bit 6 clear (64 entries + their complements);
-//   builder 1: keys with bit 6 set, e[j | 64] = e[j] + 2*x6 (it re-walks the
-//              j < 64 subtree without storing it).
+// and the live state is one value per tree level.  Builder q (0..3) owns
+// the keys whose bits 5 and 6 equal (q & 1, q >> 1):
+//     e[j | q<<5] = (e[j] (+ 2*x5)) (+ 2*x6)      for j < 32,
+// the recurrence's own order (it re-walks the j < 32 subtree).
 __device__ __forceinline__ void sts_pair(uint32_t col, int k, float v) {
     sts_f32(col + static_cast<uint32_t>(k) * 256u, v);
     sts_f32(col + static_cast<uint32_t>(kTable - 1 - k) * 256u, -v);
 }
 
-template <int K, int I, bool HI>
+template <int K, int I, int Q>
 struct Dfs {
-    // the children of node K through bits I .. 5
+    // the children of node K through bits I .. 4
     static __device__ __forceinline__ void children(float v, const float (&s)[kMU], uint32_t col) {
-        if constexpr (I < 6) {
-            Dfs<(K | (1 << I)), I + 1, HI>::node(fadd_rn(v, s[I]), s, col);
-            Dfs<K, I + 1, HI>::children(v, s, col);
+        if constexpr (I < 5) {
+            Dfs<(K | (1 << I)), I + 1, Q>::node(fadd_rn(v, s[I]), s, col);
+            Dfs<K, I + 1, Q>::children(v, s, col);
         }
     }
     static __device__ __forceinline__ void node(float v, const float (&s)[kMU], uint32_t col) {
-        if constexpr (HI) {
-            sts_pair(col, K | 64, fadd_rn(v, s[6]));
-        } else {
-            sts_pair(col, K, v);
-        }
+        float e = v;
+        if constexpr (Q & 1) e = fadd_rn(e, s[5]);
+        if constexpr (Q & 2) e = fadd_rn(e, s[6]);
+        sts_pair(col, K | (Q << 5), e);
         children(v, s, col);
     }
 };
@@ -114,25 +117,34 @@ __device__ __forceinline__ void build_tables(int which, uint32_t col, const floa
     for (int t = 0; t < kMU; ++t) e0 = __fsub_rn(e0, x[t]);
 #pragma unroll
     for (int t = 0; t < kMU; ++t) s[t] = 2.0f * x[t];
-    if (which == 0) {
-        Dfs<0, 0, false>::node(e0, s, col);
-    } else {
-        Dfs<0, 0, true>::node(e0, s, col);
+    switch (which) {
+        case 0: Dfs<0, 0, 0>::node(e0, s, col); break;
+        case 1: Dfs<0, 0, 1>::node(e0, s, col); break;
+        case 2: Dfs<0, 0, 2>::node(e0, s, col); break;
+        default: Dfs<0, 0, 3>::node(e0, s, col); break;
     }
 }
 
 // ---------------------------------------------------------------- gather
 // One 1 KiB chunk (32 rows x 32 groups of one plane): lane l sums its row's
 // 32 lookups (4 interleaved accumulators combined pairwise, the order of
-// gather_chunk in query_core.cuh).  IMM selects the buffer half (+128 B).
+// gather_chunk in query_core.cuh).  The shared address of lookup j is ONE
+// PRMT: byte 0 = the lane's rotated bank offset 4*((l+j) mod 32) (byte j%4
+// of rot[j/4]), byte 1 = key byte j%4 of w[j/4], bytes 2-3 = the sign of a
+// rot byte (< 128, so 0); the LUT base (64 KiB, kLutBase) and the buffer
+// half (+128 B) are the LDS immediate.
+constexpr uint32_t kLutBase = 0x10000u;
+
 template <int IMM>
-__device__ __forceinline__ float stream_gather(const uint32_t (&w)[8], const uint32_t (&goff)[32]) {
+__device__ __forceinline__ float stream_gather(const uint32_t (&w)[8], const uint32_t (&rot)[8]) {
     float acc[4];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-        const uint32_t off = __byte_perm(goff[j], w[j >> 2], 0x3200u | ((4u + (j & 3)) << 4));
+        uint32_t off;  // PTX prmt (not __byte_perm, which drops the sign-replicate bit of a selector nibble)
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(rot[j >> 2]), "r"(w[j >> 2]),
+            "r"(0x8800u | ((4u + (j & 3)) << 4) | (j & 3)));
         float e;
-        asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off), "n"(IMM));
+        asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off), "n"(kLutBase + IMM));
         acc[j & 3] = j < 4 ? e : acc[j & 3] + e;  // 0 + e == e (up to the sign of a zero sum)
     }
     return (acc[0] + acc[1]) + (acc[2] + acc[3]);
@@ -140,7 +152,7 @@ __device__ __forceinline__ float stream_gather(const uint32_t (&w)[8], const uin
 
 // beta chunks of one unit, combined with alpha in fp64 (planes ascending).
 template <int BETA, int IMM>
-__device__ __forceinline__ double stream_unit(uint32_t kbase, int lane, const uint32_t (&goff)[32],
+__device__ __forceinline__ double stream_unit(uint32_t kbase, int lane, const uint32_t (&rot)[8],
                                               const float (&a)[BETA]) {
     double s = 0.0;
 #pragma unroll
@@ -149,7 +161,7 @@ __device__ __forceinline__ double stream_unit(uint32_t kbase, int lane, const ui
         const uint32_t p = kbase + static_cast<uint32_t>(i) * 1024u + static_cast<uint32_t>(lane) * 16u;
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(p));
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+512];" : "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]) : "r"(p));
-        const float P = stream_gather<IMM>(w, goff);
+        const float P = stream_gather<IMM>(w, rot);
         s += static_cast<double>(a[i]) * static_cast<double>(P);
     }
     return s;
@@ -178,9 +190,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
     uint64_t* xfull = empty + kMaxStages;  // [2] x(c) loaded          (32 loader lanes)
-    uint64_t* xempty = xfull + 2;          // [2] x(c) consumed         (2 builders)
+    uint64_t* xempty = xfull + 2;          // [2] x(c) consumed         (kNBuild builders)
     uint64_t* afull = xempty + 2;          // [2] alpha(c) loaded       (32 loader lanes)
-    uint64_t* lfull = afull + 2;           // [2] LUT(c) built          (2 builders)
+    uint64_t* lfull = afull + 2;           // [2] LUT(c) built          (kNBuild builders)
     uint64_t* lempty = lfull + 2;          // [2] call c fully gathered (kNC consumers)
     float* xs = reinterpret_cast<float*>(smem + 1024);                    // [2][kXBlock]
     float* as = reinterpret_cast<float*>(smem + 1024 + 2 * kXBlock * 4);  // [2][BETA][U*32]
@@ -190,7 +202,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     const uint32_t hi0 = lut_abs + 0x10000u;
     const int nhi = hi0 + stage_bytes <= send ? static_cast<int>((send - hi0) / stage_bytes) : 0;
     const int nst = min(kMaxStages, nlo + nhi);
-    if (lut_abs + 0x10000u > send || nst < 2) __trap();  // layout assumption (dynamic smem starts near 0)
+    // layout assumption: dynamic shared memory starts below 64 KiB, so the
+    // LUT sits at kLutBase (the gather's LDS immediate)
+    if (lut_abs != kLutBase || lut_abs + 0x10000u > send || nst < 2) __trap();
     auto stage_addr = [&](int slot) -> uint32_t {
         return slot < nlo ? lo0 + static_cast<uint32_t>(slot) * stage_bytes
                           : hi0 + static_cast<uint32_t>(slot - nlo) * stage_bytes;
@@ -203,9 +217,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&xfull[b], 32);
-            mbar_init(&xempty[b], 2);
+            mbar_init(&xempty[b], kNBuild);
             mbar_init(&afull[b], 32);
-            mbar_init(&lfull[b], 2);
+            mbar_init(&lfull[b], kNBuild);
             mbar_init(&lempty[b], kNC);
         }
         fence_mbar_init();
@@ -322,8 +336,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         const int which = warp - kWBuild;
         for (int c = 0; c < ncalls; ++c) {
             const int buf = c & 1;
-            mbar_wait_sleep(&xfull[buf], static_cast<uint32_t>((c >> 1) & 1));
-            if (c >= 2) mbar_wait_sleep(&lempty[buf], static_cast<uint32_t>(((c >> 1) - 1) & 1));
+            mbar_wait(&xfull[buf], static_cast<uint32_t>((c >> 1) & 1));
+            if (c >= 2) mbar_wait(&lempty[buf], static_cast<uint32_t>(((c >> 1) - 1) & 1));
             build_tables(which, lut_abs + static_cast<uint32_t>(buf) * 128u + static_cast<uint32_t>(lane) * 4u,
                          xs + buf * kXBlock, lane);
             __syncwarp();
@@ -336,9 +350,13 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     }
 
     // ---------------------------------------------------------- consumers
-    uint32_t goff[32];
+    uint32_t rot[8];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) goff[j] = lut_abs | (static_cast<uint32_t>((lane + j) & 31) * 4u);
+    for (int q = 0; q < 8; ++q) {
+        rot[q] = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rot[q] |= (static_cast<uint32_t>((lane + 4 * q + b) & 31) * 4u) << (8 * b);
+    }
     pdl_wait();  // partials of the previous launch may still be read by its finaliser
     const long long MTP = static_cast<long long>(A.MT) * 32;
     // This warp's units are gu = warp, warp + kNC, ... of the CTA's (call,
@@ -369,8 +387,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             }
             mbar_wait(&full[slot], kphase);
             const uint32_t kbase = stage_addr(slot) + static_cast<uint32_t>(pos) * BETA * 1024u;
-            const double sum = buf == 0 ? stream_unit<BETA, 0>(kbase, lane, goff, a)
-                                        : stream_unit<BETA, 128>(kbase, lane, goff, a);
+            const double sum = buf == 0 ? stream_unit<BETA, 0>(kbase, lane, rot, a)
+                                        : stream_unit<BETA, 128>(kbase, lane, rot, a);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
             if (r < A.m) part[r] = static_cast<float>(sum);

@@ -879,3 +879,89 @@ extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_r
     }
     return BQG_OK;
 }
+
+namespace {
+// Process-wide per-device context for grouped host calls: a stream, event
+// pairs and grown-on-demand staging/workspace buffers, so a group's call does
+// not depend on which layer comes first.
+struct GroupContext {
+    std::mutex lock;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* d_x = nullptr;
+    size_t x_cap = 0;
+    float* d_y = nullptr;
+    size_t y_cap = 0;
+    void* d_ws = nullptr;
+    size_t ws_cap = 0;
+};
+GroupContext g_group_ctx[16];
+}  // namespace
+
+extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, const float* h_x, size_t x_rows,
+                                       size_t b, float* h_y, int exact, bqg_kernel_stats* stats) {
+    if (!layers || !h_x || !h_y) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null argument");
+    if (count == 0) return BQG_OK;
+    bqg_layer* L0 = layers[0];
+    if (!L0) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null");
+    for (size_t i = 1; i < count; ++i) {
+        const bqg_layer* L = layers[i];
+        if (!L) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null");
+        // kernel.hpp:127-131: every call of the group has the same shape
+        if (L->m != L0->m || L->n != L0->n || L->beta != L0->beta || L->mu != L0->mu)
+            return set_err(BQG_ERR_INVALID_ARGUMENT, "layers_forward: layers must share (m, n, beta, mu)");
+    }
+    int s = check_x(x_rows, b, L0->n, L0->mu, "biqgemm");
+    if (s) return s;
+    if (exact || L0->mu > 8) {
+        for (size_t i = 0; i < count; ++i) {
+            s = bqg_layer_forward_host(layers[i], h_x + i * x_rows * b, x_rows, b, h_y + i * L0->m * b, exact, stats);
+            if (s) return s;
+        }
+        return BQG_OK;
+    }
+    int dev = 0;
+    BQG_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 16) return set_err(BQG_ERR_INVALID_ARGUMENT, "layers_forward: device index >= 16");
+    GroupContext& G = g_group_ctx[dev];
+    std::lock_guard<std::mutex> g(G.lock);
+    if (!G.stream) {
+        BQG_CUDA(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking));
+        for (auto& e : G.ev) BQG_CUDA(cudaEventCreate(&e));
+    }
+    const size_t xs = x_rows * b, ys = L0->m * b;
+    s = grow(G.d_x, G.x_cap, sizeof(float) * xs * count);
+    if (s) return s;
+    s = grow(G.d_y, G.y_cap, sizeof(float) * ys * count);
+    if (s) return s;
+    s = grow(G.d_ws, G.ws_cap, bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, count));
+    if (s) return s;
+    std::vector<bqg_call> calls(count);
+    for (size_t i = 0; i < count; ++i) calls[i] = {layers[i]->d_tiled, layers[i]->d_alpha, G.d_x + i * xs, G.d_y + i * ys};
+    cudaStream_t st = G.stream;
+    if (stats) BQG_CUDA(cudaEventRecord(G.ev[0], st));
+    BQG_CUDA(cudaMemcpyAsync(G.d_x, h_x, sizeof(float) * xs * count, cudaMemcpyHostToDevice, st));
+    if (stats) BQG_CUDA(cudaEventRecord(G.ev[1], st));
+    s = bqg_biqgemm_grouped_f32(calls.data(), count, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap, 0,
+                                st);
+    if (s) return s;
+    if (stats) BQG_CUDA(cudaEventRecord(G.ev[2], st));
+    BQG_CUDA(cudaMemcpyAsync(h_y, G.d_y, sizeof(float) * ys * count, cudaMemcpyDeviceToHost, st));
+    if (stats) BQG_CUDA(cudaEventRecord(G.ev[3], st));
+    BQG_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+        uint64_t ops[4];
+        bqg_op_counters(L0->m, L0->n, b, L0->beta, L0->mu, BQG_LUT_DP, ops);
+        stats->lut_build_ops += ops[0] * count;
+        stats->lookups += ops[1] * count;
+        stats->accumulate_ops += ops[2] * count;
+        stats->fma_ops += ops[3] * count;
+        float t01 = 0, t12 = 0, t23 = 0;
+        cudaEventElapsedTime(&t01, G.ev[0], G.ev[1]);
+        cudaEventElapsedTime(&t12, G.ev[1], G.ev[2]);
+        cudaEventElapsedTime(&t23, G.ev[2], G.ev[3]);
+        stats->query_seconds += t12 * 1e-3;
+        stats->replace_seconds += (t01 + t23) * 1e-3;
+    }
+    return BQG_OK;
+}

@@ -112,3 +112,38 @@ def test_grouped_rejects_bad_arguments(bq, cuda):
         bq.biqgemm_grouped_device(entries, 256, 64, 256, 1, 2, 8, small)
     with pytest.raises(_capi.InvalidArgument):
         bq.biqgemm_grouped_device(entries, 257, 64, 256, 1, 2, 8, ws)  # x longer than G*mu
+
+
+def test_layers_forward_host(bq, port, cuda):
+    """bqg_layers_forward_host: host x/y for a group of layers (one H2D, the
+    grouped kernels, one D2H) equals each layer's own forward bitwise in the
+    stream form's contract, and the exact path reproduces the reference."""
+    m, n, beta = 300, 1000, 3
+    layers = [bq.PackedLinear.from_weights(bq.random_uniform(m, n, 40 + i), beta, 8) for i in range(5)]
+    x = np.stack([bq.random_normal(n, 1, 90 + i) for i in range(5)])
+    y = bq.layers_forward(layers, x)
+    y_exact = bq.layers_forward(layers, x, exact=True)
+    stats = bq.KernelStats()
+    bq.layers_forward(layers, x, stats=stats)
+    assert stats.lookups == 5 * m * ((n + 7) // 8) * beta
+    for i, L in enumerate(layers):
+        keys, alpha = L.export()
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x[i])
+        assert_close(y[i], y_ref)
+        assert np.array_equal(y_exact[i], L.forward(x[i], exact=True))
+    # grouped host call == grouped device call (same kernels, bitwise)
+    import torch
+
+    entries = [(torch.from_numpy(bq.tile_keys(torch.from_numpy(L.export()[0]).cuda(), n, 8).cpu().numpy()).cuda(),
+                torch.from_numpy(L.export()[1]).cuda(), torch.from_numpy(x[i]).cuda(), torch.empty((m, 1), device="cuda"))
+               for i, L in enumerate(layers)]
+    ws = bq.grouped_workspace(m, n, 1, beta, 8, 5)
+    bq.biqgemm_grouped_device(entries, n, m, n, 1, beta, 8, ws)
+    torch.cuda.synchronize()
+    for i, e in enumerate(entries):
+        assert np.array_equal(e[3].cpu().numpy(), y[i])
+    with pytest.raises(Exception):
+        bq.layers_forward(layers + [bq.PackedLinear.from_weights(bq.random_uniform(m + 1, n, 1), beta, 8)],
+                          np.concatenate([x, x[:1]]))
+    for L in layers:
+        L.close()

@@ -17,7 +17,7 @@ seen = set()
 for r in rows[2:]:
     try:
         ex, st = float(r[i_ex] or 0), float(r[i_st] or 0)
-    except ValueError:
+    except (ValueError, IndexError):
         continue
     if r[0] in seen:
         break  # second copy of the same kernel
