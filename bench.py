@@ -240,6 +240,15 @@ def run_ours(args):
             dist.barrier()
         return e0.elapsed_time(e1)
 
+    if args.profile:
+        # under ncu: W warm-up calls and one timed replay, nothing else
+        with torch.cuda.stream(stream):
+            g_warm.replay()
+            g_timed.replay()
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "config": args.config, "steps": args.steps, "group": G}))
+        return
     with ClockSampler(local_rank) as clk:
         # warm-up steps + enough untimed replays for steady clocks (>= 1 s,
         # and until the sampler has readings under load)
@@ -463,6 +472,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--group", type=int, default=128, help="independent calls per grouped launch")
+    ap.add_argument("--profile", action="store_true", help="for ncu: warm-up + one timed replay only, no JSON line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -56,14 +56,15 @@ constexpr int kTable = 1 << kMU;
 #define BQG_STREAM_NC 18
 #endif
 constexpr int kNC = BQG_STREAM_NC;               // consumer (gather) warps
-constexpr int kWKey = kNC, kWLoad = kNC + 1;     // key-stream warp, x/alpha loader warp
-constexpr int kWBuild = kNC + 2;                 // LUT builder warps
+constexpr int kWKey = kNC;                       // key-stream warp
+constexpr int kWX = kNC + 1, kWA = kNC + 2;      // x loader, alpha loader
+constexpr int kWBuild = kNC + 3;                 // LUT builder warps
 constexpr int kNBuild = 4;
-constexpr int kSThreads = (kNC + 2 + kNBuild) * 32;
+constexpr int kSThreads = (kNC + 3 + kNBuild) * 32;
+constexpr uint32_t kAlphaBudget = 48 * 1024;     // all alpha buffers together
 constexpr int kMaxStages = 24;
 constexpr int kStreamSmem = 227 * 1024;          // opt-in maximum per CTA
 constexpr int kXBlock = 32 * kMU;                // x rows per group block
-constexpr int kAlphaBudget = 48 * 1024;          // both alpha buffers together
 
 struct StreamArgs {
     int ncalls;
@@ -179,32 +180,50 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     const int U = static_cast<int>(static_cast<long long>(jb + 1) * A.MT / A.cpb) - t0;
     const long long u0 = static_cast<long long>(gb) * A.MT + t0;
     const int ncalls = A.ncalls;
-    const long long total_units = static_cast<long long>(ncalls) * U;
+    const int spc = (U + A.ups - 1) / A.ups;  // ring stages per call
+    // alpha of the CTA's rows, staged per call in nab buffers ([BETA][U*32]):
+    // 4 when they fit the budget (loads run up to 3 calls ahead), else 2; if
+    // even 2 do not fit, gather warps load alpha themselves
     const uint32_t abuf_bytes = static_cast<uint32_t>(U) * BETA * 128u;
-    const bool alpha_smem = 2u * abuf_bytes <= static_cast<uint32_t>(kAlphaBudget);
+    // (2 buffers: measured faster than 4 -- the key ring keeps the room)
+    const int nab = 2;
+    const bool alpha_smem = static_cast<uint32_t>(nab) * abuf_bytes <= kAlphaBudget;
 
-    // ---- shared memory: [bars | x bufs | alpha bufs | stages.. | LUT 64K | ..stages]
+    // ---- shared memory:
+    //   [bars 1K | x bufs 4x1K | alpha bufs | stages.. | LUT 64K | ..stages]
+    // LUT buffer lb = (64 KiB region lb/2, half lb%2); the code supports up to
+    // 4 buffers (two regions), the kernel uses nlb = 2.
     const uint32_t sbase = smem_u32(smem);
     const uint32_t lut_abs = (sbase + 0xFFFFu) & ~0xFFFFu;
     const uint32_t send = sbase + kStreamSmem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
-    uint64_t* xfull = empty + kMaxStages;  // [2] x(c) loaded          (32 loader lanes)
-    uint64_t* xempty = xfull + 2;          // [2] x(c) consumed         (kNBuild builders)
-    uint64_t* afull = xempty + 2;          // [2] alpha(c) loaded       (32 loader lanes)
-    uint64_t* lfull = afull + 2;           // [2] LUT(c) built          (kNBuild builders)
-    uint64_t* lempty = lfull + 2;          // [2] call c fully gathered (kNC consumers)
-    float* xs = reinterpret_cast<float*>(smem + 1024);                    // [2][kXBlock]
-    float* as = reinterpret_cast<float*>(smem + 1024 + 2 * kXBlock * 4);  // [2][BETA][U*32]
+    uint64_t* xfull = empty + kMaxStages;  // [4] x(c) loaded                (32 x-loader lanes)
+    uint64_t* xempty = xfull + 4;          // [4] x(c) consumed               (kNBuild builders)
+    uint64_t* lfull = xempty + 4;          // [4] LUT(c) built                (kNBuild builders)
+    uint64_t* ldone = lfull + 4;           // [4] call c gathered: LUT free   (kNC consumers)
+    uint64_t* afull = ldone + 4;           // [4] alpha(c) loaded             (32 alpha-loader lanes)
+    uint64_t* adone = afull + 4;           // [4] call c gathered: alpha free (kNC consumers)
+    // issued[slot] = 1 + the ring round last issued into the slot (release by
+    // the key warp, acquire by a consumer before its parity wait on full[]):
+    // slots refill independently, so without it a warp far ahead could wait
+    // on a slot two rounds early, which the mbarrier parity cannot tell apart
+    uint32_t* issued = reinterpret_cast<uint32_t*>(adone + 4);  // [kMaxStages]
+    float* xs = reinterpret_cast<float*>(smem + 1024);                    // [4][kXBlock]
+    float* as = reinterpret_cast<float*>(smem + 1024 + 4 * kXBlock * 4);  // [nab][BETA][U*32]
     const uint32_t stage_bytes = static_cast<uint32_t>(A.ups) * BETA * 1024u;
-    const uint32_t lo0 = (sbase + 1024u + 2u * kXBlock * 4u + (alpha_smem ? 2u * abuf_bytes : 0u) + 127u) & ~127u;
+    const uint32_t lo0 =
+        (sbase + 1024u + 4u * kXBlock * 4u + (alpha_smem ? static_cast<uint32_t>(nab) * abuf_bytes : 0u) + 127u) & ~127u;
     const int nlo = lo0 + stage_bytes <= lut_abs ? static_cast<int>((lut_abs - lo0) / stage_bytes) : 0;
-    const uint32_t hi0 = lut_abs + 0x10000u;
-    const int nhi = hi0 + stage_bytes <= send ? static_cast<int>((send - hi0) / stage_bytes) : 0;
-    const int nst = min(kMaxStages, nlo + nhi);
+    auto nhi_at = [&](uint32_t hi) { return hi + stage_bytes <= send ? static_cast<int>((send - hi) / stage_bytes) : 0; };
+    // 2 LUT buffers (the halves of one 64 KiB region); 4 (a second region)
+    // is supported by the protocol but measured slower: ring bytes matter more
+    const int nlb = 2;
+    const uint32_t hi0 = lut_abs + (nlb == 4 ? 0x20000u : 0x10000u);
+    const int nst = min(kMaxStages, nlo + nhi_at(hi0));
     // layout assumption: dynamic shared memory starts below 64 KiB, so the
     // LUT sits at kLutBase (the gather's LDS immediate)
-    if (lut_abs != kLutBase || lut_abs + 0x10000u > send || nst < 2) __trap();
+    if (lut_abs != kLutBase || hi0 > send || nst < 2) __trap();
     auto stage_addr = [&](int slot) -> uint32_t {
         return slot < nlo ? lo0 + static_cast<uint32_t>(slot) * stage_bytes
                           : hi0 + static_cast<uint32_t>(slot - nlo) * stage_bytes;
@@ -215,63 +234,64 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], A.ups);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 4; ++b) {
             mbar_init(&xfull[b], 32);
             mbar_init(&xempty[b], kNBuild);
-            mbar_init(&afull[b], 32);
             mbar_init(&lfull[b], kNBuild);
-            mbar_init(&lempty[b], kNC);
+            mbar_init(&ldone[b], kNC);
         }
+        for (int b = 0; b < 4; ++b) {
+            mbar_init(&afull[b], 32);
+            mbar_init(&adone[b], kNC);
+        }
+        for (int s = 0; s < kMaxStages; ++s) issued[s] = 0;
         fence_mbar_init();
     }
     __syncthreads();
 
     if (warp == kWKey) {
         // ---------------------------------------------------- key stream
+        // Stages are call-aligned: call c's U units fill spc = ceil(U/ups)
+        // stages (the last one possibly partial), stage s = c*spc + j.
         // Lane L owns ring slot L (stages L, L+nst, ...): the bulk copies of
         // different stages are issued by different lanes, in parallel (one
         // issuing thread caps the copy rate at ~3 TB/s chip-wide with 8-12
         // KiB copies; several reach ~7 TB/s: tools/ubench/tma_stream.cu).
+        // The issued-round guard (issued[]) is what keeps the protocol sound;
+        // stages need no gating on the calls' LUT/alpha readiness
+        // (tools/stream_protocol_sim.py models the protocol).
         if (lane < nst) {
             const uint64_t pol = policy_evict_first();
-            const long long nstages_total = (total_units + A.ups - 1) / A.ups;
+            const long long nstages_total = static_cast<long long>(ncalls) * spc;
             for (long long s = lane; s < nstages_total; s += nst) {
                 const int slot = lane;
                 const long long round = s / nst;
                 if (round > 0) mbar_wait_sleep(&empty[slot], static_cast<uint32_t>((round - 1) & 1));
-                const long long g0 = s * A.ups, g1 = min(g0 + A.ups, total_units);
-                mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(g1 - g0) * BETA * 1024u);
-                long long g = g0;
-                while (g < g1) {
-                    const int c = static_cast<int>(g / U);
-                    const int k = static_cast<int>(g - static_cast<long long>(c) * U);
-                    const int len = static_cast<int>(min(static_cast<long long>(U - k), g1 - g));
-                    const unsigned char* src = A.calls[c].keys + (u0 + k) * BETA * 1024;
-                    const uint32_t dst = stage_addr(slot) + static_cast<uint32_t>(g - g0) * BETA * 1024u;
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-                        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                        "l"(src), "r"(static_cast<uint32_t>(len) * BETA * 1024u), "r"(smem_u32(&full[slot])),
-                        "l"(pol)
-                        : "memory");
-                    g += len;
-                }
+                const int c = static_cast<int>(s / spc), j = static_cast<int>(s - static_cast<long long>(c) * spc);
+                const int k0 = j * A.ups, len = min(A.ups, U - k0);
+                const uint32_t bytes = static_cast<uint32_t>(len) * BETA * 1024u;
+                mbar_arrive_expect_tx(&full[slot], bytes);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+                    "[%0], [%1], %2, [%3], %4;" ::"r"(stage_addr(slot)),
+                    "l"(A.calls[c].keys + (u0 + k0) * BETA * 1024), "r"(bytes), "r"(smem_u32(&full[slot])), "l"(pol)
+                    : "memory");
+                asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&issued[slot])),
+                             "r"(static_cast<uint32_t>(round + 1))
+                             : "memory");
             }
         }
         return;
     }
-    if (warp == kWLoad) {
-        // -------------------------------- x(c) and alpha(c), ahead of use
-        // TMA bulk copies when the rows are 16-byte aligned and complete;
-        // otherwise the 32 lanes copy (zero-filling rows past x_rows / m).
+    if (warp == kWX) {
+        // ------------------------------ x(c) into buffer c%4, ahead of use
+        // TMA bulk copy when the block's rows are 16-byte aligned and
+        // complete; otherwise the 32 lanes copy (zero past x_rows).
         pdl_wait();
         const long long r0 = static_cast<long long>(gb) * kXBlock;
-        const long long ra = static_cast<long long>(t0) * 32;
-        const long long arows = min(static_cast<long long>(U) * 32, static_cast<long long>(A.m) - ra);
         for (int c = 0; c < ncalls; ++c) {
-            const int buf = c & 1;
-            const uint32_t par = static_cast<uint32_t>(((c >> 1) - 1) & 1);  // phase of call c-2
-            if (c >= 2) mbar_wait_sleep(&xempty[buf], par);
+            const int buf = c & 3;
+            if (c >= 4) mbar_wait_sleep(&xempty[buf], static_cast<uint32_t>(((c >> 2) - 1) & 1));
             const float* x = A.calls[c].x;
             float* xd = xs + buf * kXBlock;
             if (r0 + kXBlock <= A.x_rows && (reinterpret_cast<uintptr_t>(x + r0) & 15) == 0) {
@@ -292,10 +312,21 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
                 for (int q = 0; q < kXBlock / 32; ++q) xd[q * 32 + lane] = v[q];
                 mbar_arrive(&xfull[buf]);
             }
+        }
+        return;
+    }
+    if (warp == kWA) {
+        // ------------------------- alpha(c) into buffer c % nab ([BETA][U*32])
+        const long long ra = static_cast<long long>(t0) * 32;
+        const long long arows = min(static_cast<long long>(U) * 32, static_cast<long long>(A.m) - ra);
+        for (int c = 0; c < ncalls; ++c) {
+            const int buf = c % nab;
+            // afull runs at most nab phases ahead of the consumers (even when
+            // alpha is not staged), so its parity waits never alias
+            if (c >= nab) mbar_wait_sleep(&adone[buf], static_cast<uint32_t>((c / nab - 1) & 1));
             if (alpha_smem) {
-                if (c >= 2) mbar_wait_sleep(&lempty[buf], par);
                 const float* al = A.calls[c].alpha;
-                float* ad = as + buf * (abuf_bytes / 4);  // [BETA][U*32]
+                float* ad = as + buf * (abuf_bytes / 4);
                 const uint32_t nbytes = static_cast<uint32_t>(arows) * 4u;
                 const bool tma = al && (nbytes & 15) == 0 && (A.m & 3) == 0 &&
                                  (reinterpret_cast<uintptr_t>(al + ra) & 15) == 0;
@@ -332,18 +363,19 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         return;
     }
     if (warp >= kWBuild) {
-        // ------------------------------------------- LUT(c) into half c&1
+        // ------------------------------------ LUT(c) into buffer c % nlb
         const int which = warp - kWBuild;
         for (int c = 0; c < ncalls; ++c) {
-            const int buf = c & 1;
-            mbar_wait(&xfull[buf], static_cast<uint32_t>((c >> 1) & 1));
-            if (c >= 2) mbar_wait(&lempty[buf], static_cast<uint32_t>(((c >> 1) - 1) & 1));
-            build_tables(which, lut_abs + static_cast<uint32_t>(buf) * 128u + static_cast<uint32_t>(lane) * 4u,
-                         xs + buf * kXBlock, lane);
+            const int lb = c % nlb, xb = c & 3;
+            mbar_wait(&xfull[xb], static_cast<uint32_t>((c >> 2) & 1));
+            if (c >= nlb) mbar_wait(&ldone[lb], static_cast<uint32_t>((c / nlb - 1) & 1));
+            build_tables(which, lut_abs + static_cast<uint32_t>(lb >> 1) * 0x10000u + static_cast<uint32_t>(lb & 1) * 128u +
+                                    static_cast<uint32_t>(lane) * 4u,
+                         xs + xb * kXBlock, lane);
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&xempty[buf]);
-                mbar_arrive(&lfull[buf]);
+                mbar_arrive(&xempty[xb]);
+                mbar_arrive(&lfull[lb]);
             }
         }
         return;
@@ -360,53 +392,75 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     pdl_wait();  // partials of the previous launch may still be read by its finaliser
     const long long MTP = static_cast<long long>(A.MT) * 32;
     // This warp's units are gu = warp, warp + kNC, ... of the CTA's (call,
-    // unit) sequence; their ring position (stage slot, unit in stage,
-    // phase) advances incrementally -- no divisions in the loop.
+    // unit) sequence (continuous across calls: balanced however U and kNC
+    // relate).  Unit k of call c is in stage c*spc + k/ups at position
+    // k%ups; the ring slot and phase advance incrementally.
     int gu = warp;
-    int pos = gu % A.ups, slot = (gu / A.ups) % nst;
-    uint32_t kphase = static_cast<uint32_t>((gu / A.ups) / nst) & 1u;
-    const int adv_q = kNC / A.ups, adv_r = kNC - (kNC / A.ups) * A.ups;
+    long long st_cur = 0;  // global stage index that (slot, kround) describe
+    int slot = 0;
+    uint32_t kround = 0;
     for (int c = 0; c < ncalls; ++c) {
-        const int buf = c & 1;
-        const uint32_t par = static_cast<uint32_t>((c >> 1) & 1);
-        mbar_wait(&lfull[buf], par);
-        mbar_wait(&afull[buf], par);
+        const int lb = c % nlb;
+        const int ab_i = c % nab;
+        mbar_wait(&lfull[lb], static_cast<uint32_t>((c / nlb) & 1));
+        mbar_wait(&afull[ab_i], static_cast<uint32_t>((c / nab) & 1));
         const float* alpha = A.calls[c].alpha;
-        const float* ab = as + buf * (abuf_bytes / 4);
+        const float* ab = as + ab_i * (abuf_bytes / 4);
         float* part = A.partial + (static_cast<long long>(c) * A.NB + gb) * MTP;
         const int cbase = c * U;
         for (; gu < cbase + U; gu += kNC) {
             const int k = gu - cbase;
             const long long r = static_cast<long long>(t0 + k) * 32 + lane;
+            const int sj = k / A.ups, pos = k - sj * A.ups;
             float a[BETA];
 #pragma unroll
             for (int i = 0; i < BETA; ++i) {
                 if (alpha_smem) a[i] = ab[(i * U + k) * 32 + lane];
-                else if (alpha) a[i] = r < A.m ? __ldg(alpha + static_cast<long long>(i) * A.m + r) : 0.0f;
-                else a[i] = 1.0f;
+                else a[i] = alpha ? (r < A.m ? __ldg(alpha + static_cast<long long>(i) * A.m + r) : 0.0f) : 1.0f;
             }
-            mbar_wait(&full[slot], kphase);
+            const long long st = static_cast<long long>(c) * spc + sj;
+            {
+                long long d = st - st_cur;
+                if (d >= nst) {
+                    slot = static_cast<int>(st % nst);
+                    kround = static_cast<uint32_t>(st / nst);
+                } else {
+                    slot += static_cast<int>(d);
+                    if (slot >= nst) {
+                        slot -= nst;
+                        ++kround;
+                    }
+                }
+                st_cur = st;
+            }
+            {
+                uint32_t iss;
+                do {
+                    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(iss) : "r"(smem_u32(&issued[slot])) : "memory");
+                } while (iss <= kround);
+            }
+            mbar_wait(&full[slot], kround & 1u);
             const uint32_t kbase = stage_addr(slot) + static_cast<uint32_t>(pos) * BETA * 1024u;
-            const double sum = buf == 0 ? stream_unit<BETA, 0>(kbase, lane, rot, a)
-                                        : stream_unit<BETA, 128>(kbase, lane, rot, a);
+            double sum;
+            switch (lb) {
+                case 0: sum = stream_unit<BETA, 0>(kbase, lane, rot, a); break;
+                case 1: sum = stream_unit<BETA, 128>(kbase, lane, rot, a); break;
+                case 2: sum = stream_unit<BETA, 0x10000>(kbase, lane, rot, a); break;
+                default: sum = stream_unit<BETA, 0x10080>(kbase, lane, rot, a); break;
+            }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (lane == 0) {
+                // the last unit of a partial (call-final) stage completes its count
+                const int nin = min(A.ups, U - sj * A.ups);
+                mbar_arrive_cnt(&empty[slot], pos == nin - 1 ? static_cast<uint32_t>(A.ups - nin + 1) : 1u);
+            }
             if (r < A.m) part[r] = static_cast<float>(sum);
-            // advance the ring position by kNC units
-            pos += adv_r;
-            int adv = adv_q;
-            if (pos >= A.ups) {
-                pos -= A.ups;
-                ++adv;
-            }
-            slot += adv;
-            if (slot >= nst) {
-                slot -= nst;
-                kphase ^= 1u;
-            }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&lempty[buf]);
+        if (lane == 0) {
+            mbar_arrive(&ldone[lb]);
+            mbar_arrive(&adone[ab_i]);
+        }
     }
 }
 
@@ -478,7 +532,10 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
     // tiles of that block; one CTA per SM when NB <= #SMs
     A.cpb = std::max(1, std::min(A.MT, sms / A.NB));
     A.grid = A.cpb * A.NB;
-    A.ups = std::max(1, 12 / beta);  // ~12 KiB ring stages
+#ifndef BQG_STREAM_STAGE_KB
+#define BQG_STREAM_STAGE_KB 16
+#endif
+    A.ups = std::max(1, BQG_STREAM_STAGE_KB / beta);  // ~16 KiB ring stages (TMA bulk copies)
     A.partial = ws;
     for (int done = 0; done < count; done += kStreamMaxGroup) {
         A.ncalls = std::min(kStreamMaxGroup, count - done);
