@@ -1,37 +1,27 @@
-"""Summarise ncu captures into profiles/ (tracked): per-kernel duration,
-DRAM bytes, throughput and stall breakdown, plus profiles/ncu_summary.json
-(read by bench.py for roofline.traffic).
+"""Summarise a round's ncu evidence into profiles/ (tracked):
 
-    python tools/summarize_ncu.py <round-tag> <config>=<report.ncu-rep> ... [--launches <csv>]
+  profiles/ncu_<tag>.md          per-config full-capture metrics of the hot
+                                 kernel, stall breakdown, launch-list shares
+  profiles/ncu_launches_<tag>_<cfg>.csv   the launch lists themselves
+  profiles/ncu_summary.json      per-config DRAM bytes per launch (bench.py
+                                 reads it for roofline.traffic)
+
+    python tools/summarize_ncu.py <tag> <dir with full_<cfg>.ncu-rep and launches_<cfg>.csv> <cfg> [<cfg> ...]
 """
 import csv
 import json
+import shutil
 import subprocess
 import sys
+from collections import defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 PROF = ROOT / "profiles"
+sys.path.insert(0, str(ROOT))
 
-
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3,
-         "msecond": 1e6, "ms": 1e6,
-         "second": 1e9}
-
-
-def raw_metrics(rep):
-    """Rows of the raw page with values converted to base units (bytes, ns)."""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    hdr, units = rows[0], rows[1]
-    kernels = []
-    for r in rows[2:]:
-        d = {}
-        for h, u, v in zip(hdr, units, r):
-            f = fnum(v)
-            d[h] = f * SCALE[u] if (f is not None and u in SCALE) else v
-        kernels.append(d)
-    return kernels
+SCALE = {"us": 1e3, "ns": 1, "ms": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+         "second": 1e9, "Tbyte/s": 1e12, "Gbyte/s": 1e9, "Mbyte/s": 1e6, "Ghz": 1e9, "Mhz": 1e6}
 
 
 def fnum(v):
@@ -41,56 +31,102 @@ def fnum(v):
         return None
 
 
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {}
+        for h, u, v in zip(hdr, units, r):
+            f = fnum(v)
+            d[h] = f * SCALE.get(u, 1) if f is not None else v
+        res.append(d)
+    return res
+
+
+def launch_shares(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ik, iv, im, iid = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name"), h.index("ID")
+    per = defaultdict(dict)
+    for r in rows[hi + 1:]:
+        if len(r) > max(ik, iv, im, iid):
+            per[(r[iid], r[ik])][r[im]] = fnum(r[iv])
+    agg = defaultdict(lambda: [0, 0.0, 0.0])
+    for (_, name), v in per.items():
+        a = agg[name.split("(")[0][:70]]
+        a[0] += 1
+        a[1] += v.get("gpu__time_duration.sum") or 0
+        a[2] += (v.get("dram__bytes_read.sum") or 0)
+    return agg
+
+
 def main():
-    tag = sys.argv[1]
-    args = sys.argv[2:]
-    launches = None
-    if "--launches" in args:
-        i = args.index("--launches")
-        launches = args[i + 1]
-        args = args[:i] + args[i + 2:]
+    tag, d = sys.argv[1], Path(sys.argv[2])
+    cfgs = sys.argv[3:]
+    from bench import CONFIGS, key_bytes
+
     PROF.mkdir(exist_ok=True)
-    summary_path = PROF / "ncu_summary.json"
-    summary = json.loads(summary_path.read_text()) if summary_path.exists() else {}
-    lines = [f"# ncu summary, round {tag}", ""]
-    for a in args:
-        cfg, rep = a.split("=", 1)
-        for k in raw_metrics(rep):
-            name = k.get("Kernel Name", "?")
-            dur_ns = fnum(k.get("gpu__time_duration.sum"))
-            rd = fnum(k.get("dram__bytes_read.sum"))
-            wr = fnum(k.get("dram__bytes_write.sum"))
-            # ncu reports bytes in scaled units in raw csv units row; normalise by the unit row if present
-            d = {
-                "kernel": name[:120],
-                "duration_us": dur_ns / 1000 if dur_ns else None,
-                "dram_read_bytes": rd,
-                "dram_write_bytes": wr,
-                "sm_throughput_pct": fnum(k.get("sm__throughput.avg.pct_of_peak_sustained_elapsed")),
-                "dram_throughput_pct": fnum(k.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")),
-                "lsu_shared_wavefronts": fnum(k.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")),
-                "registers": fnum(k.get("launch__registers_per_thread")),
-                "grid": k.get("launch__grid_size"),
-            }
-            lines.append(f"## {cfg}: {name[:100]}")
-            for kk, vv in d.items():
-                lines.append(f"- {kk}: {vv}")
-            lines.append("")
-            if "biqgemm" in name:
-                summary[cfg] = {"dram_bytes_per_launch": (rd or 0) + (wr or 0), "duration_us_ncu": d["duration_us"],
-                                "kernel": d["kernel"], "round": tag}
-    if launches:
-        lines.append("## launch list (ncu --metrics gpu__time_duration.sum, cold cache, serialised)")
-        with open(launches) as f:
-            rows = [r for r in csv.reader(f) if len(r) > 10]
-        hdr = rows[0]
-        for r in rows[1:]:
-            rec = dict(zip(hdr, r))
-            if rec.get("Metric Name") == "gpu__time_duration.sum":
-                lines.append(f"- {rec.get('Kernel Name', '?')[:90]}: {rec.get('Metric Value')} ns")
-    (PROF / f"ncu_{tag}.md").write_text("\n".join(lines) + "\n")
-    summary_path.write_text(json.dumps(summary, indent=1) + "\n")
-    print("\n".join(lines[:60]))
+    sp = PROF / "ncu_summary.json"
+    summary = json.loads(sp.read_text()) if sp.exists() else {}
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    L = [f"# ncu evidence, round {tag}", "",
+         "Captured with tools/profile_round.sh under gpurun on one B200: `ncu --set full --clock-control none "
+         "--import-source on -k regex:biqgemm_stream_kernel -s 2 -c 1` of `python bench.py --config <C> --profile "
+         "--steps 512 --warmup 3` (one grouped launch = 128 independent calls), and the launch list "
+         "(`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`, cold-cache, serialised: "
+         "compare shares, not absolutes).", ""]
+    for cfg in cfgs:
+        m, n, beta, b, mu = CONFIGS[cfg]
+        kb = key_bytes(m, n, beta, mu)
+        rep = d / f"full_{cfg}.ncu-rep"
+        if rep.exists():
+            for k in raw(rep):
+                name = k.get("Kernel Name", "?")
+                if "biqgemm_stream_kernel" not in name:
+                    continue
+                dur = k.get("gpu__time_duration.sum")
+                rd, wr = k.get("dram__bytes_read.sum") or 0, k.get("dram__bytes_write.sum") or 0
+                calls = 128
+                alg = kb * calls
+                lsu = k.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") or 0
+                sms = k.get("launch__grid_size")
+                clk = k.get("sm__cycles_elapsed.avg.per_second")
+                L += [f"## {cfg} (m={m} n={n} q={beta} mu={mu} b={b}): `biqgemm_stream_kernel<{beta}>`", "",
+                      "| metric | value |", "|---|---|",
+                      f"| duration (one launch, {calls} calls) | {dur / 1e3:.1f} us = {dur / 1e3 / calls:.3f} us/call |",
+                      f"| algorithmic key bytes / launch | {alg / 1e6:.1f} MB ({kb} B/call) |",
+                      f"| achieved (algorithmic) | {alg / dur:.0f} GB/s = {alg / dur / peaks.get('hbm_gbs', 6536.4) * 100:.1f}% of {peaks.get('hbm_gbs', 6536.4)} GB/s measured peak |",
+                      f"| DRAM read / write | {rd / 1e6:.1f} MB / {wr / 1e6:.1f} MB (read/algorithmic = {rd / alg:.3f}) |",
+                      f"| DRAM throughput | {k.get('dram__bytes_read.sum.per_second', 0) / 1e12:.2f} TB/s read |",
+                      f"| shared-memory wavefronts | {lsu / 1e6:.2f} M = {lsu / calls / max(sms or 1, 1):.0f} per CTA per call |",
+                      f"| LSU pipe busy | {k.get('sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active')} % |",
+                      f"| issue active | {k.get('smsp__issue_active.avg.pct_of_peak_sustained_active')} % |",
+                      f"| SM clock under ncu | {clk / 1e9 if clk else None} GHz |",
+                      f"| registers / threads / grid | {k.get('launch__registers_per_thread')} / {k.get('launch__block_size')} / {sms} |",
+                      ""]
+                stalls = sorted(((h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""), v)
+                                 for h, v in k.items() if h.startswith("smsp__average_warps_issue_stalled")
+                                 and "not_issued" not in h and isinstance(v, float) and v > 0.05), key=lambda t: -t[1])
+                L += ["Stalls per issued instruction: " + ", ".join(f"{a} {v:.2f}" for a, v in stalls[:8]), ""]
+                summary[cfg] = {"dram_bytes_per_launch": rd + wr, "calls_per_launch": calls,
+                                "algorithmic_bytes_per_launch": alg, "duration_us_ncu": dur / 1e3,
+                                "kernel": name[:100], "round": tag}
+        lp = d / f"launches_{cfg}.csv"
+        if lp.exists():
+            shutil.copy(lp, PROF / f"ncu_launches_{tag}_{cfg}.csv")
+            agg = launch_shares(lp)
+            tot = sum(a[1] for a in agg.values()) or 1
+            L += [f"### {cfg} launch list (whole bench --profile run, incl. setup kernels)", "",
+                  "| kernel | launches | time us | share | DRAM read MB |", "|---|---|---|---|---|"]
+            for nm, (c, t, rb) in sorted(agg.items(), key=lambda x: -x[1][1]):
+                L.append(f"| `{nm}` | {c} | {t / 1e3:.1f} | {t / tot * 100:.1f}% | {rb / 1e6:.1f} |")
+            L.append("")
+    (PROF / f"ncu_{tag}.md").write_text("\n".join(L) + "\n")
+    sp.write_text(json.dumps(summary, indent=1) + "\n")
+    print("\n".join(L))
 
 
 if __name__ == "__main__":
