@@ -45,6 +45,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "lut_build.cuh"  // Log2
 
 namespace bqg {
 
@@ -59,7 +60,10 @@ constexpr int kNC = BQG_STREAM_NC;               // consumer (gather) warps
 constexpr int kWKey = kNC;                       // key-stream warp
 constexpr int kWX = kNC + 1, kWA = kNC + 2;      // x loader, alpha loader
 constexpr int kWBuild = kNC + 3;                 // LUT builder warps
-constexpr int kNBuild = 4;
+#ifndef BQG_STREAM_NBUILD
+#define BQG_STREAM_NBUILD 4
+#endif
+constexpr int kNBuild = BQG_STREAM_NBUILD;       // 1, 2, 4 or 8
 constexpr int kSThreads = (kNC + 3 + kNBuild) * 32;
 constexpr uint32_t kAlphaBudget = 48 * 1024;     // all alpha buffers together
 constexpr int kMaxStages = 24;
@@ -82,34 +86,37 @@ struct StreamArgs {
 // and the second half its negation, e[255 - k] = -e[k] (lut.hpp:63-66).  The
 // recurrence tree is walked depth-first at compile time (parent -> child =
 // one fadd), so every entry is produced by exactly the reference's addition
-// and the live state is one value per tree level.  Builder q (0..3) owns
-// the keys whose bits 5 and 6 equal (q & 1, q >> 1):
-//     e[j | q<<5] = (e[j] (+ 2*x5)) (+ 2*x6)      for j < 32,
-// the recurrence's own order (it re-walks the j < 32 subtree).
+// and the live state is one value per tree level.  With NB builder warps
+// (NB = 2^h, h <= 3), builder q owns the keys whose top h first-half bits
+// (bits 7-h .. 6) equal q:
+//     e[j | q << (7-h)] = ((e[j] (+ 2*x_{7-h})) ...) (+ 2*x6)     for j < 2^(7-h),
+// the recurrence's own order (each builder re-walks the j < 2^(7-h) subtree).
 __device__ __forceinline__ void sts_pair(uint32_t col, int k, float v) {
     sts_f32(col + static_cast<uint32_t>(k) * 256u, v);
     sts_f32(col + static_cast<uint32_t>(kTable - 1 - k) * 256u, -v);
 }
 
-template <int K, int I, int Q>
+template <int K, int I, int Q, int LB>  // LB = low bits walked by the DFS (7 - h)
 struct Dfs {
-    // the children of node K through bits I .. 4
     static __device__ __forceinline__ void children(float v, const float (&s)[kMU], uint32_t col) {
-        if constexpr (I < 5) {
-            Dfs<(K | (1 << I)), I + 1, Q>::node(fadd_rn(v, s[I]), s, col);
-            Dfs<K, I + 1, Q>::children(v, s, col);
+        if constexpr (I < LB) {
+            Dfs<(K | (1 << I)), I + 1, Q, LB>::node(fadd_rn(v, s[I]), s, col);
+            Dfs<K, I + 1, Q, LB>::children(v, s, col);
         }
     }
     static __device__ __forceinline__ void node(float v, const float (&s)[kMU], uint32_t col) {
         float e = v;
-        if constexpr (Q & 1) e = fadd_rn(e, s[5]);
-        if constexpr (Q & 2) e = fadd_rn(e, s[6]);
-        sts_pair(col, K | (Q << 5), e);
+#pragma unroll
+        for (int t = LB; t < 7; ++t)
+            if ((Q >> (t - LB)) & 1) e = fadd_rn(e, s[t]);
+        sts_pair(col, K | (Q << LB), e);
         children(v, s, col);
     }
 };
 
+template <int NBW>
 __device__ __forceinline__ void build_tables(int which, uint32_t col, const float* xb, int lane) {
+    constexpr int LB = 7 - Log2<NBW>::value;
     float x[kMU], s[kMU];
 #pragma unroll
     for (int t = 0; t < kMU; ++t) x[t] = xb[lane * kMU + t];
@@ -119,10 +126,14 @@ __device__ __forceinline__ void build_tables(int which, uint32_t col, const floa
 #pragma unroll
     for (int t = 0; t < kMU; ++t) s[t] = 2.0f * x[t];
     switch (which) {
-        case 0: Dfs<0, 0, 0>::node(e0, s, col); break;
-        case 1: Dfs<0, 0, 1>::node(e0, s, col); break;
-        case 2: Dfs<0, 0, 2>::node(e0, s, col); break;
-        default: Dfs<0, 0, 3>::node(e0, s, col); break;
+        case 0: Dfs<0, 0, 0, LB>::node(e0, s, col); break;
+        case 1: if constexpr (NBW > 1) Dfs<0, 0, 1, LB>::node(e0, s, col); break;
+        case 2: if constexpr (NBW > 2) Dfs<0, 0, 2, LB>::node(e0, s, col); break;
+        case 3: if constexpr (NBW > 3) Dfs<0, 0, 3, LB>::node(e0, s, col); break;
+        case 4: if constexpr (NBW > 4) Dfs<0, 0, 4, LB>::node(e0, s, col); break;
+        case 5: if constexpr (NBW > 5) Dfs<0, 0, 5, LB>::node(e0, s, col); break;
+        case 6: if constexpr (NBW > 6) Dfs<0, 0, 6, LB>::node(e0, s, col); break;
+        default: if constexpr (NBW > 7) Dfs<0, 0, 7, LB>::node(e0, s, col); break;
     }
 }
 
@@ -137,18 +148,52 @@ __device__ __forceinline__ void build_tables(int which, uint32_t col, const floa
 constexpr uint32_t kLutBase = 0x10000u;
 
 template <int IMM>
+__device__ __forceinline__ float lds_lut(uint32_t rotw, uint32_t w, uint32_t sel) {
+    uint32_t off;  // PTX prmt (not __byte_perm, which drops the sign-replicate bit of a selector nibble)
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(rotw), "r"(w), "r"(sel));
+    float e;
+    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off), "n"(kLutBase + IMM));
+    return e;
+}
+
+// The 4 interleaved accumulators acc[j % 4] are kept as two f32x2 pairs
+// (acc0, acc1) and (acc2, acc3): one FADD2 adds lookups j and j+1 of the same
+// 4-step group -- the same additions, in the same order, as 4 scalar chains.
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float2 unpack2(uint64_t a) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(a));
+    return r;
+}
+
+template <int IMM>
 __device__ __forceinline__ float stream_gather(const uint32_t (&w)[8], const uint32_t (&rot)[8]) {
-    float acc[4];
+    uint64_t acc01 = 0, acc23 = 0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        uint32_t off;  // PTX prmt (not __byte_perm, which drops the sign-replicate bit of a selector nibble)
-        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(rot[j >> 2]), "r"(w[j >> 2]),
-            "r"(0x8800u | ((4u + (j & 3)) << 4) | (j & 3)));
-        float e;
-        asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off), "n"(kLutBase + IMM));
-        acc[j & 3] = j < 4 ? e : acc[j & 3] + e;  // 0 + e == e (up to the sign of a zero sum)
+    for (int q = 0; q < 8; ++q) {  // lookups j = 4q .. 4q+3
+        const float e0 = lds_lut<IMM>(rot[q], w[q], 0x8840u);
+        const float e1 = lds_lut<IMM>(rot[q], w[q], 0x8851u);
+        const float e2 = lds_lut<IMM>(rot[q], w[q], 0x8862u);
+        const float e3 = lds_lut<IMM>(rot[q], w[q], 0x8873u);
+        if (q == 0) {  // 0 + e == e (up to the sign of a zero sum)
+            acc01 = pack2(e0, e1);
+            acc23 = pack2(e2, e3);
+        } else {
+            acc01 = fadd2(acc01, pack2(e0, e1));
+            acc23 = fadd2(acc23, pack2(e2, e3));
+        }
     }
-    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    const float2 a = unpack2(acc01), b = unpack2(acc23);
+    return (a.x + a.y) + (b.x + b.y);
 }
 
 // beta chunks of one unit, combined with alpha in fp64 (planes ascending).
@@ -369,7 +414,7 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             const int lb = c % nlb, xb = c & 3;
             mbar_wait(&xfull[xb], static_cast<uint32_t>((c >> 2) & 1));
             if (c >= nlb) mbar_wait(&ldone[lb], static_cast<uint32_t>((c / nlb - 1) & 1));
-            build_tables(which, lut_abs + static_cast<uint32_t>(lb >> 1) * 0x10000u + static_cast<uint32_t>(lb & 1) * 128u +
+            build_tables<kNBuild>(which, lut_abs + static_cast<uint32_t>(lb >> 1) * 0x10000u + static_cast<uint32_t>(lb & 1) * 128u +
                                     static_cast<uint32_t>(lane) * 4u,
                          xs + xb * kXBlock, lane);
             __syncwarp();

@@ -45,7 +45,7 @@ struct StreamCall {
     const float* x;       // x_rows x 1
     float* y;             // m x 1
 };
-constexpr int kStreamMaxGroup = 128;  // calls per launch (kernel-parameter array)
+constexpr int kStreamMaxGroup = 512;  // calls per launch (kernel-parameter array, 16 KiB)
 bool stream_supported(int mu, int beta, long long b);
 size_t stream_workspace_bytes(long long m, long long groups, int count);
 cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,

@@ -74,7 +74,7 @@ def grouped_graph(gsize, ws):
     return gg
 
 
-for gsize in sorted({1, 8, 32, group}):
+for gsize in sorted({1, 32, 128, group}):
     ws = bq.grouped_workspace(m, n, b, beta, mu, gsize)
     gg = grouped_graph(gsize, ws)
     gg.replay()
