@@ -158,6 +158,12 @@ int bqg_biqgemm_f32(const uint8_t* d_keys_tiled, const float* d_alpha, const flo
                     size_t x_rows, float* d_y, size_t m, size_t n, size_t b, unsigned beta,
                     unsigned mu, void* d_workspace, size_t workspace_bytes, int pdl, void* stream);
 
+/* Which single-call kernel form bqg_biqgemm_f32 uses for this shape on the
+ * current device: 1 = latency form (b == 1, mu == 8, beta <= 4, n <= 4096:
+ * one kernel, in-cluster push reduction, y bitwise equal to the grouped
+ * form), 2 = cluster form, 3 = two-kernel form; 0 = no fast path. */
+int bqg_biqgemm_form(size_t m, size_t n, size_t b, unsigned beta, unsigned mu);
+
 /* Grouped calls: `count` independent biqgemm calls (kernel.hpp:246-258, one
  * per entry) that share (m, n, b, beta, mu) but have their own weights,
  * alpha, x and y -- the Q/K/V or gate/up projections of one layer, or one

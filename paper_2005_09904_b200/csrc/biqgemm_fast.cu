@@ -355,6 +355,17 @@ int plan_cpb(long long m, long long groups, int beta, long long b, int num_sms) 
     return make_plan(m, groups, beta, b, 8, num_sms).cpb;
 }
 
+int fast_form(const QueryParams& p, int mu) {
+    static const int debug_flags = [] {
+        const char* e = getenv("BQG_DEBUG_FLAGS");
+        return e ? atoi(e) : 0;
+    }();
+    if (!(debug_flags & (128 | 8192 | 16384)) && latency_supported(mu, p.beta, p.b, p.NB) && latency_applies(p)) return 1;
+    const bool cluster_shape = p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
+    if (!(debug_flags & 128) && (cluster_shape || (debug_flags & 8192))) return 2;  // (if the device can co-schedule it)
+    return 3;
+}
+
 cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaStream_t stream) {
     static const int debug_flags = [] {
         const char* e = getenv("BQG_DEBUG_FLAGS");  // profiling switches; never set in production
@@ -371,6 +382,11 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
     // The single-kernel cluster form wins when the per-call fixed costs
     // dominate and one column tile covers b (measured: C2 6.6 vs 8.5 us); the
     // two-kernel form (148 CTAs, cost-model split) wins for larger b / m.
+    if (!(debug_flags & (128 | 8192 | 16384)) && latency_supported(mu, p.beta, p.b, p.NB)) {  // 16384: skip (profiling)
+        bool used = false;
+        cudaError_t e = launch_biqgemm_latency(p, pdl, stream, &used);
+        if (e != cudaSuccess || used) return e;
+    }
     const bool cluster_shape = p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
     if (!(debug_flags & 128) && (cluster_shape || (debug_flags & 8192))) {  // 128/8192: force a form (profiling)
         bool used = false;

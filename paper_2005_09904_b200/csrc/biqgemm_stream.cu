@@ -239,7 +239,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     // LUT buffer lb = (64 KiB region lb/2, half lb%2); the code supports up to
     // 4 buffers (two regions), the kernel uses nlb = 2.
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t lut_abs = (sbase + 0xFFFFu) & ~0xFFFFu;
+    // the LUT sits at offset kLutBase of the CTA's shared window (the
+    // gather's LDS immediate); no cluster here, so no rank bits
+    const uint32_t lut_abs = (sbase & 0xFF000000u) | kLutBase;
     const uint32_t send = sbase + kStreamSmem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     const int nst = min(kMaxStages, nlo + nhi_at(hi0));
     // layout assumption: dynamic shared memory starts below 64 KiB, so the
     // LUT sits at kLutBase (the gather's LDS immediate)
-    if (lut_abs != kLutBase || hi0 > send || nst < 2) __trap();
+    if (sbase > lut_abs || lo0 > lut_abs || hi0 > send || nst < 2) __trap();
     auto stage_addr = [&](int slot) -> uint32_t {
         return slot < nlo ? lo0 + static_cast<uint32_t>(slot) * stage_bytes
                           : hi0 + static_cast<uint32_t>(slot - nlo) * stage_bytes;

@@ -538,6 +538,13 @@ extern "C" int bqg_biqgemm_grouped_f32(const bqg_call* h_calls, size_t count, si
     return BQG_OK;
 }
 
+extern "C" int bqg_biqgemm_form(size_t m, size_t n, size_t b, unsigned beta, unsigned mu) {
+    if (mu < 1 || mu > 8 || m == 0 || n == 0 || b == 0 || beta == 0) return 0;
+    if (ensure_device() != BQG_OK) return 0;
+    const bqg::QueryParams p = make_params(nullptr, nullptr, nullptr, n, nullptr, m, n, b, beta, mu, nullptr);
+    return bqg::fast_form(p, static_cast<int>(mu));
+}
+
 extern "C" size_t bqg_biqgemm_exact_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu) {
     if (mu < 1 || mu > 16 || m == 0 || n == 0 || b == 0 || beta == 0) return 0;
     return bqg::exact_workspace_bytes(static_cast<long long>(m), static_cast<long long>(n), static_cast<int>(beta),

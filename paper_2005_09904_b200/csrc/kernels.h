@@ -51,6 +51,15 @@ size_t stream_workspace_bytes(long long m, long long groups, int count);
 cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
                                   float* ws, bool pdl, cudaStream_t stream);
 
+// Single-call latency form (biqgemm_latency.cu): b == 1, mu == 8, beta <= 4,
+// NB in {1,2,4,8,16}; one kernel, in-cluster push reduction.  *used = false
+// when the shape does not fit (caller falls back).
+bool latency_supported(int mu, int beta, long long b, int NB);
+cudaError_t launch_biqgemm_latency(const QueryParams& p, bool pdl, cudaStream_t stream, bool* used);
+bool latency_applies(const QueryParams& p);
+// Which single-call form launch_biqgemm_fast picks: 1 latency, 2 cluster, 3 two-kernel.
+int fast_form(const QueryParams& p, int mu);
+
 // Workspace for the fast path (bytes).
 size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b);
 // Grid planner: CTAs per 32-group block.

@@ -147,3 +147,34 @@ def test_layers_forward_host(bq, port, cuda):
                           np.concatenate([x, x[:1]]))
     for L in layers:
         L.close()
+
+
+@pytest.mark.parametrize("m,n,beta", [(1, 8, 1), (33, 7, 2), (100, 300, 3), (1000, 777, 4), (4096, 4096, 3),
+                                      (2000, 4096, 1), (16384, 4096, 3), (70, 2048, 2), (5000, 1024, 3)])
+def test_single_call_latency_form_matches_stream_form(bq, port, cuda, m, n, beta):
+    """The single-call latency kernel (b == 1, mu == 8) uses the stream form's
+    arithmetic: y is bitwise identical to a grouped call of one, and within
+    the fp32 contract of the reference."""
+    import torch
+
+    entries, host = make_group(bq, torch, 1, m, n, beta, 8, 300 + m)
+    y_stream = run_group(bq, entries, n, m, n, 1, beta, 8)[0]
+    tiled, a, x, _ = entries[0]
+    y = torch.full((m, 1), float("nan"), device="cuda")
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, 1, beta, 8)))
+    bq.biqgemm_device(tiled, a, x, y, m, n, beta, 8, ws)
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    if bq.lib.bqg_biqgemm_form(m, n, 1, beta, 8) == 1:  # the latency form ran
+        assert np.array_equal(y, y_stream)
+    else:
+        assert_close(y, y_stream.astype(np.float64), tol=1e-6)
+    keys, alpha, xh = host[0]
+    y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, xh)
+    assert_close(y, y_ref)
+    # short x (zero-padded rows) and plane mode
+    xs = torch.from_numpy(bq.random_normal(n - 5 if n > 5 else n, 1, 7)).cuda()
+    bq.biqgemm_device(tiled, None, xs, y_t := torch.empty((m, 1), device="cuda"), m, n, beta, 8, ws)
+    torch.cuda.synchronize()
+    y_ref2, _ = port.biqgemm(keys.astype(np.uint32), None, n, 8, xs.cpu().numpy())
+    assert_close(y_t.cpu().numpy(), y_ref2)
