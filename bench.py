@@ -150,9 +150,17 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, local_rank, world = dist_env()
+    # BQG_BENCH_BACKEND=gloo + BQG_BENCH_ONE_DEVICE=1: exercise the multi-rank
+    # control flow on one GPU (test only; the driver's runs use NCCL, one GPU per rank)
+    backend = os.environ.get("BQG_BENCH_BACKEND", "nccl")
+    if os.environ.get("BQG_BENCH_ONE_DEVICE") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     import paper_2005_09904_b200.biqgemm as bq
 
     m, n, beta, b, mu = CONFIGS[args.config]
@@ -255,9 +263,16 @@ def run_ours(args):
         with torch.cuda.stream(stream):
             g_warm.replay()
             t0 = time.perf_counter()
-            while time.perf_counter() - t0 < 1.0 or (len(clk.samples) < 3 and time.perf_counter() - t0 < 10):
+            while True:
                 g_timed.replay()
                 stream.synchronize()
+                more = time.perf_counter() - t0 < 1.0 or (len(clk.samples) < 3 and time.perf_counter() - t0 < 10)
+                if world > 1:
+                    flag = torch.tensor([1.0 if more else 0.0], device=dev)
+                    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+                    more = bool(flag.item() > 0)
+                if not more:
+                    break
         n_before = len(clk.samples)
         ms = 0.0
         reps = 0
@@ -265,9 +280,16 @@ def run_ours(args):
         # barrier + synchronize; repeated (>= 3 times, and until the sampler
         # has read the clocks during timed work); the MEDIAN replay is reported
         times = []
-        while reps < 3 or (len(clk.samples) <= n_before and reps < 200):
+        while True:
             times.append(timed(g_timed))
             reps += 1
+            more = reps < 3 or (len(clk.samples) <= n_before and reps < 200)
+            if world > 1:  # every rank runs the same number of (barrier-bracketed) replays
+                flag = torch.tensor([1.0 if more else 0.0], device=dev)
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+                more = bool(flag.item() > 0)
+            if not more:
+                break
         ms = float(np.median(times))
         clocks = clk.summary(since=n_before)
 
