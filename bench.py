@@ -25,9 +25,9 @@ in GB/s; us/call is reported beside it.
 each PDL-chained behind its predecessor (consecutive layers of one model).
 
 e2e: the same calls through the public C ABI with HOST buffers
-(bqg_layers_forward_host per group of G calls: one H2D of the G inputs from
-pinned memory, the grouped kernels, one D2H of the G outputs, synchronised),
-wall-clock timed.
+(bqg_layers_forward_host per 512 calls: H2D of the inputs from pinned
+memory, the grouped kernels, D2H of the outputs -- pipelined inside the call
+in 64-call sub-groups on separate streams -- synchronised), wall-clock timed.
 
 N>1 (torchrun): weak scaling -- every rank owns a C2-sized row shard of an
 (N*4096) x 4096 layer, and y is assembled with an NCCL all-gather each step.
@@ -334,10 +334,11 @@ def run_ours(args):
     # of G calls one bqg_layers_forward_host = H2D of the G inputs, the
     # grouped kernels, D2H of the G outputs, synchronised
     e2e_layers = [layer] + [bq.PackedLinear.from_keys(keys, alpha, n, mu) for _ in range(copies - 1)]
-    x_pin = torch.from_numpy(np.stack([x_h[i % copies] for i in range(G)])).pin_memory()
-    y_pin = torch.empty((G, m, b), dtype=torch.float32).pin_memory()
-    groups = [[e2e_layers[(st + i) % copies] for i in range(min(G, args.steps - st))]
-              for st in range(0, args.steps, G)]
+    GE = args.e2e_group  # calls per synchronised API call (the library pipelines copies inside it)
+    x_pin = torch.from_numpy(np.stack([x_h[i % copies] for i in range(GE)])).pin_memory()
+    y_pin = torch.empty((GE, m, b), dtype=torch.float32).pin_memory()
+    groups = [[e2e_layers[(st + i) % copies] for i in range(min(GE, args.steps - st))]
+              for st in range(0, args.steps, GE)]
     for grp in groups[:2]:
         bq.layers_forward_into(grp, x_pin[:len(grp)], y_pin[:len(grp)])
     if world > 1:
@@ -388,7 +389,8 @@ def run_ours(args):
                     "form": "dependent-call regime: one single-call kernel per step, PDL-chained CUDA graph"},
         "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": int(x_h[0].nbytes),
                 "d2h_bytes_per_step": int(m * b * 4), "us_per_call": e2e_s / args.steps * 1e6,
-                "api": f"bqg_layers_forward_host, {G} calls per synchronised API call"},
+                "api": f"bqg_layers_forward_host, {GE} calls per synchronised API call "
+                       "(H2D / kernels / D2H pipelined in 64-call sub-groups inside the call)"},
         "gpu_launches": 2 * n_launch if stream_form else args.steps * 2,
         "clocks": clocks,
         "parity_rel_fro": rel,
@@ -494,6 +496,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--group", type=int, default=128, help="independent calls per grouped launch")
+    ap.add_argument("--e2e-group", type=int, default=512, help="calls per bqg_layers_forward_host call (e2e leg)")
     ap.add_argument("--profile", action="store_true", help="for ncu: warm-up + one timed replay only, no JSON line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

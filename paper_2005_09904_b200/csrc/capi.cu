@@ -891,10 +891,14 @@ namespace {
 // Process-wide per-device context for grouped host calls: a stream, event
 // pairs and grown-on-demand staging/workspace buffers, so a group's call does
 // not depend on which layer comes first.
+constexpr int kChunkEv = 8;
 struct GroupContext {
     std::mutex lock;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t copy = nullptr;    // H2D
+    cudaStream_t down = nullptr;    // D2H
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t chunk_ev[kChunkEv] = {};
     float* d_x = nullptr;
     size_t x_cap = 0;
     float* d_y = nullptr;
@@ -934,28 +938,49 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
     std::lock_guard<std::mutex> g(G.lock);
     if (!G.stream) {
         BQG_CUDA(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking));
+        BQG_CUDA(cudaStreamCreateWithFlags(&G.copy, cudaStreamNonBlocking));
+        BQG_CUDA(cudaStreamCreateWithFlags(&G.down, cudaStreamNonBlocking));
         for (auto& e : G.ev) BQG_CUDA(cudaEventCreate(&e));
+        for (auto& e : G.chunk_ev) BQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     const size_t xs = x_rows * b, ys = L0->m * b;
     s = grow(G.d_x, G.x_cap, sizeof(float) * xs * count);
     if (s) return s;
     s = grow(G.d_y, G.y_cap, sizeof(float) * ys * count);
     if (s) return s;
-    s = grow(G.d_ws, G.ws_cap, bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, count));
+    // Pipelined in sub-groups of kSub calls: the H2D of sub-group k+1 (copy
+    // stream) and the D2H of sub-group k-1 (down stream) overlap the kernels
+    // of sub-group k (compute stream).  y is the same as one grouped call.
+    constexpr size_t kSub = 64;
+    const size_t nsub = (count + kSub - 1) / kSub;
+    s = grow(G.d_ws, G.ws_cap,
+             bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, std::min(count, kSub)));
     if (s) return s;
     std::vector<bqg_call> calls(count);
     for (size_t i = 0; i < count; ++i) calls[i] = {layers[i]->d_tiled, layers[i]->d_alpha, G.d_x + i * xs, G.d_y + i * ys};
-    cudaStream_t st = G.stream;
-    if (stats) BQG_CUDA(cudaEventRecord(G.ev[0], st));
-    BQG_CUDA(cudaMemcpyAsync(G.d_x, h_x, sizeof(float) * xs * count, cudaMemcpyHostToDevice, st));
-    if (stats) BQG_CUDA(cudaEventRecord(G.ev[1], st));
-    s = bqg_biqgemm_grouped_f32(calls.data(), count, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap, 0,
-                                st);
-    if (s) return s;
-    if (stats) BQG_CUDA(cudaEventRecord(G.ev[2], st));
-    BQG_CUDA(cudaMemcpyAsync(h_y, G.d_y, sizeof(float) * ys * count, cudaMemcpyDeviceToHost, st));
-    if (stats) BQG_CUDA(cudaEventRecord(G.ev[3], st));
+    cudaStream_t st = G.stream, cp = G.copy, dp = G.down;
+    if (stats) BQG_CUDA(cudaEventRecord(G.ev[0], cp));
+    for (size_t k = 0; k < nsub; ++k) {
+        const size_t i0 = k * kSub, cnt = std::min(kSub, count - i0);
+        cudaEvent_t h2d = G.chunk_ev[(2 * k) % kChunkEv], done = G.chunk_ev[(2 * k + 1) % kChunkEv];
+        BQG_CUDA(cudaMemcpyAsync(G.d_x + i0 * xs, h_x + i0 * xs, sizeof(float) * xs * cnt, cudaMemcpyHostToDevice, cp));
+        BQG_CUDA(cudaEventRecord(h2d, cp));
+        BQG_CUDA(cudaStreamWaitEvent(st, h2d, 0));
+        if (stats && k == 0) BQG_CUDA(cudaEventRecord(G.ev[1], st));
+        s = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap, 0,
+                                    st);
+        if (s) return s;
+        BQG_CUDA(cudaEventRecord(done, st));
+        BQG_CUDA(cudaStreamWaitEvent(dp, done, 0));
+        BQG_CUDA(cudaMemcpyAsync(h_y + i0 * ys, G.d_y + i0 * ys, sizeof(float) * ys * cnt, cudaMemcpyDeviceToHost, dp));
+    }
+    if (stats) {
+        BQG_CUDA(cudaEventRecord(G.ev[2], st));
+        BQG_CUDA(cudaEventRecord(G.ev[3], dp));
+    }
+    BQG_CUDA(cudaStreamSynchronize(dp));
     BQG_CUDA(cudaStreamSynchronize(st));
+    BQG_CUDA(cudaStreamSynchronize(cp));
     if (stats) {
         uint64_t ops[4];
         bqg_op_counters(L0->m, L0->n, b, L0->beta, L0->mu, BQG_LUT_DP, ops);
@@ -963,12 +988,12 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
         stats->lookups += ops[1] * count;
         stats->accumulate_ops += ops[2] * count;
         stats->fma_ops += ops[3] * count;
-        float t01 = 0, t12 = 0, t23 = 0;
+        float t01 = 0, t12 = 0, t03 = 0;
         cudaEventElapsedTime(&t01, G.ev[0], G.ev[1]);
         cudaEventElapsedTime(&t12, G.ev[1], G.ev[2]);
-        cudaEventElapsedTime(&t23, G.ev[2], G.ev[3]);
+        cudaEventElapsedTime(&t03, G.ev[0], G.ev[3]);
         stats->query_seconds += t12 * 1e-3;
-        stats->replace_seconds += (t01 + t23) * 1e-3;
+        stats->replace_seconds += (t03 - t12 > 0 ? t03 - t12 : 0) * 1e-3;
     }
     return BQG_OK;
 }
