@@ -48,7 +48,8 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 constexpr int kMU = 8;
 constexpr int kTable = 1 << kMU;
-constexpr int kLW = 16;                    // warps per CTA (all build, all gather)
+constexpr int kLW = 18;                    // warps per CTA (all gather; the first 16 build)
+constexpr int kLB = 16;                    // builder warps
 constexpr int kLThreads = kLW * 32;
 constexpr int kPieceChunks = 8;            // 8 KiB per key copy
 constexpr int kMaxPieces = 32;
@@ -291,9 +292,9 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
     pdl_wait();  // x of the predecessor is visible from here on
     if (tl) g_timeline_lat[blockIdx.x][2] = gtime();
 
-    // ---- LUT: bpc blocks, 16 / bpc builder warps each
-    {
-        const int b = warp / (kLW / bpc), which = warp - b * (kLW / bpc);
+    // ---- LUT: bpc blocks, kLB / bpc builder warps each
+    if (warp < kLB) {
+        const int b = warp / (kLB / bpc), which = warp - b * (kLB / bpc);
         const uint32_t col = lut_abs + static_cast<uint32_t>(b) * 128u + static_cast<uint32_t>(lane) * 4u;
         const int gb = s_rank * bpc + b;
         if (bpc == 1) build_share<16>(which, col, A.x, A.x_rows, gb, lane);
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
     __syncthreads();
     if (tl) g_timeline_lat[blockIdx.x][3] = gtime();
 
-    // ---- gather: chunk q = (block b, tile k, plane i), warps take q = w, w+16, ...
+    // ---- gather: chunk q = (block b, tile k, plane i), warps take q = w, w+kLW, ...
     for (int q = warp; q < nchunk; q += kLW) {
         const int b = q / nchunk_b, c = q - b * nchunk_b;
         mbar_wait(&kbar[b * npb + c / kPieceChunks], 0);
