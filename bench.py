@@ -397,6 +397,8 @@ def run_ours(args):
     }
     if world > 1:
         line["allgather_ms_total"] = gather_ms
+    if world == 1 and not args.no_comparators:
+        line["comparators"] = comparators(bq, layer, w_shard, x_h, m, n, beta, b, mu, kb, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, keys, alpha, x_h[0], m, n, beta, mu, b, args.cpu_seconds)
     if rank == 0:
@@ -405,6 +407,71 @@ def run_ours(args):
         L.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def comparators(bq, layer, w, x_h, m, n, beta, b, mu, kb, dev, calls=200):
+    """The paper's comparison points on this GPU (Table IV
+    analog), device-timed per call with rotating copies > 2x L2: cuBLAS dense
+    GEMV on the dequantized weights (fp32 and bf16), the reference's
+    unpack-then-multiply method (gemm_unpack, GPU kernel) and the packed-word
+    bandwidth probe.  Each is a reference point, not the product."""
+    import torch
+
+    out = {}
+    s = torch.cuda.Stream(device=dev)
+
+    def timeit(fns):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            for f in fns[:3]:
+                f()
+            s.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                for f in fns:
+                    f()
+            g.replay()
+            s.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+        s.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / len(fns)
+
+    keys, alpha, planes = layer.export(planes=True)
+    wq = np.zeros((m, n), np.float32)  # dequantize(q) (quantize.hpp:61-74): sum_i alpha_i * B_i
+    bits = np.unpackbits(planes.view(np.uint8).reshape(beta, m, -1), axis=2, bitorder="little")[:, :, :n]
+    for i in range(beta):
+        wq += alpha[i][:, None] * (2.0 * bits[i] - 1.0).astype(np.float32)
+    x_d = [torch.from_numpy(x).to(dev) for x in x_h[:4]]
+    for name, dt in (("cublas_fp32_gemv", torch.float32), ("cublas_bf16_gemv", torch.bfloat16)):
+        w0 = torch.from_numpy(wq).to(dev).to(dt)
+        nc = int(np.ceil(2 * L2_BYTES / (w0.numel() * w0.element_size()))) + 1
+        ws_ = [w0] + [w0.clone() for _ in range(nc - 1)]
+        xs_ = [xx.to(dt) for xx in x_d]
+        ys_ = [torch.empty((m, b), device=dev, dtype=dt) for _ in range(nc)]
+        us = timeit([(lambda j=j: torch.matmul(ws_[j % nc], xs_[j % 4], out=ys_[j % nc])) for j in range(calls)])
+        wbytes = w0.numel() * w0.element_size()
+        out[name] = {"us_per_call": round(us, 3), "weight_bytes": int(wbytes),
+                     "weight_gbs": round(wbytes / (us * 1e-6) / 1e9, 1)}
+        del ws_
+    p0 = torch.from_numpy(planes.view(np.int32)).to(dev)
+    nc = int(np.ceil(2 * L2_BYTES / (p0.numel() * 4))) + 1
+    ps = [p0] + [p0.clone() for _ in range(nc - 1)]
+    al = torch.from_numpy(alpha).to(dev)
+    yy = [torch.empty((m, b), device=dev) for _ in range(nc)]
+    if b <= 8 and n * b * 4 <= 200 * 1024:
+        us = timeit([(lambda j=j: bq.gemm_unpack_device(ps[j % nc], al, x_d[j % 4], yy[j % nc], m, n, beta,
+                                                        stream=torch.cuda.current_stream().cuda_stream))
+                     for j in range(calls)])
+        out["gemm_unpack_gpu"] = {"us_per_call": round(us, 3), "key_gbs": round(kb / (us * 1e-6) / 1e9, 1)}
+    po = torch.empty(1184 * 512, device=dev)
+    us = timeit([(lambda j=j: bq.bandwidth_probe_device(ps[j % nc], beta * m, n, x_d[0], po,
+                                                        stream=torch.cuda.current_stream().cuda_stream))
+                 for j in range(calls)])
+    out["bandwidth_probe_gpu"] = {"us_per_call": round(us, 3), "key_gbs": round(kb / (us * 1e-6) / 1e9, 1),
+                                  "what": "streaming read of the packed sign words (the key-stream roofline)"}
+    return out
 
 
 # ------------------------------------------------------------ CPU reference
@@ -495,6 +562,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-comparators", action="store_true", help="skip the cuBLAS / unpack / probe reference points")
     ap.add_argument("--group", type=int, default=128, help="independent calls per grouped launch")
     ap.add_argument("--e2e-group", type=int, default=512, help="calls per bqg_layers_forward_host call (e2e leg)")
     ap.add_argument("--profile", action="store_true", help="for ncu: warm-up + one timed replay only, no JSON line")

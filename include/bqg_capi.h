@@ -200,6 +200,18 @@ int bqg_biqgemm_exact_f64(const void* d_keys, const double* d_alpha, const doubl
                           size_t x_rows, double* d_y, size_t m, size_t n, size_t b, unsigned beta,
                           unsigned mu, void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Comparison baselines on the GPU (reference baselines.hpp; not the BiQGEMM
+ * path).  gemm_unpack (baselines.hpp:40-52): y = sum_i alpha_i * (B_i x)
+ * straight from the sign-plane words (beta x m x ceil(n/32) u32, bit 1 =
+ * +1), fp32, b <= 8 and n*b*4 <= 200 KiB.  bandwidth_probe
+ * (baselines.hpp:65-87): one multiply-add per packed word (values
+ * meaningless); streaming != 0 reads the words with coalesced 16-byte loads
+ * and writes one value per thread of a 1184 x 512 grid into d_out. */
+int bqg_gemm_unpack_f32(const uint32_t* d_planes, const float* d_alpha, const float* d_x, size_t x_rows,
+                        float* d_y, size_t m, size_t n, size_t b, unsigned beta, void* stream);
+int bqg_bandwidth_probe(const uint32_t* d_words, size_t m, size_t n, const float* d_x, size_t x_rows,
+                        float* d_out, int streaming, void* stream);
+
 /* ------------------------------------------------------------ layer handle
  * A device-resident PackedLinear<float> (kernel.hpp:217-241) with its
  * workspace and a private stream: what the reference's callers hold. */

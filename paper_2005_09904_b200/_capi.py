@@ -88,6 +88,8 @@ SIGNATURES = {
     "bqg_biqgemm_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
     "bqg_biqgemm_grouped_workspace_bytes": (sz, [sz, sz, sz, u32, u32, sz]),
     "bqg_biqgemm_form": (i32, [sz, sz, sz, u32, u32]),
+    "bqg_gemm_unpack_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, vp]),
+    "bqg_bandwidth_probe": (i32, [vp, sz, sz, vp, sz, vp, i32, vp]),
     "bqg_biqgemm_grouped_f32": (i32, [vp, sz, sz, sz, sz, sz, u32, u32, vp, sz, i32, vp]),
     "bqg_layers_forward_host": (i32, [vp, sz, vp, sz, sz, vp, i32, vp]),
     "bqg_biqgemm_exact_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),

@@ -243,6 +243,21 @@ def biqgemm_grouped_device(calls, x_rows, m, n, b, beta, mu, workspace: Workspac
                                       workspace.ptr(), workspace.nbytes, 1 if pdl else 0, _stream(stream)))
 
 
+def gemm_unpack_device(planes, alpha, x, y, m, n, beta, stream=None):
+    """Reference baseline gemm_unpack (baselines.hpp:40-52) on the GPU: planes [beta, m, ceil(n/32)] u32."""
+    x_rows, b = x.shape
+    check(lib.bqg_gemm_unpack_f32(_ptr(planes), _ptr(alpha) if alpha is not None else None, _ptr(x), x_rows, _ptr(y),
+                                  m, n, b, beta, _stream(stream)))
+    return y
+
+
+def bandwidth_probe_device(words, m, n, x, out, streaming=True, stream=None):
+    """Reference baseline gemm_bandwidth_probe (baselines.hpp:65-87): packed-word traffic only."""
+    check(lib.bqg_bandwidth_probe(_ptr(words), m, n, _ptr(x), x.shape[0], _ptr(out), 1 if streaming else 0,
+                                  _stream(stream)))
+    return out
+
+
 def biqgemm_exact_device(keys, alpha, x, y, m, n, beta, mu, stream=None):
     """Exact path (fp64, bit-identical to the reference) on device tensors; keys row-major."""
     x_rows, b = x.shape

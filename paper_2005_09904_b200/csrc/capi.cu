@@ -586,6 +586,36 @@ extern "C" int bqg_biqgemm_exact_f64(const void* d_keys, const double* d_alpha, 
     return biqgemm_exact_impl<double>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, d_ws, ws_bytes, stream);
 }
 
+// ============================================================== comparison baselines
+
+extern "C" int bqg_gemm_unpack_f32(const uint32_t* d_planes, const float* d_alpha, const float* d_x, size_t x_rows,
+                                   float* d_y, size_t m, size_t n, size_t b, unsigned beta, void* stream) {
+    int s = check_dims(m, n, "gemm_unpack");
+    if (s) return s;
+    if (beta == 0 || b == 0 || b > 8 || x_rows == 0 || x_rows > n || n * b * 4 > 200 * 1024)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "gemm_unpack: needs 1 <= b <= 8, x_rows <= n, n*b*4 <= 200 KiB");
+    if (!d_planes || !d_x || !d_y) return set_err(BQG_ERR_INVALID_ARGUMENT, "gemm_unpack: null pointer");
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_gemm_unpack(d_planes, d_alpha, d_x, static_cast<long long>(x_rows), d_y,
+                                            static_cast<long long>(m), static_cast<long long>(n), static_cast<int>(b),
+                                            static_cast<int>(beta), as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "gemm_unpack kernel");
+    return BQG_OK;
+}
+
+extern "C" int bqg_bandwidth_probe(const uint32_t* d_words, size_t m, size_t n, const float* d_x, size_t x_rows,
+                                   float* d_out, int streaming, void* stream) {
+    int s = check_dims(m, n, "gemm_bandwidth_probe");
+    if (s) return s;
+    if (!d_words || !d_x || !d_out || x_rows == 0) return set_err(BQG_ERR_INVALID_ARGUMENT, "bandwidth_probe: bad argument");
+    BQG_NEED_DEVICE();
+    cudaError_t e = bqg::launch_bandwidth_probe(d_words, static_cast<long long>(m), static_cast<long long>(n), d_x,
+                                                static_cast<long long>(x_rows), d_out, streaming != 0,
+                                                as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "bandwidth_probe kernel");
+    return BQG_OK;
+}
+
 // ============================================================== layer handle
 
 struct bqg_layer {

@@ -60,6 +60,12 @@ bool latency_applies(const QueryParams& p);
 // Which single-call form launch_biqgemm_fast picks: 1 latency, 2 cluster, 3 two-kernel.
 int fast_form(const QueryParams& p, int mu);
 
+// Comparison baselines (baselines.cu; reference baselines.hpp:40-87).
+cudaError_t launch_gemm_unpack(const uint32_t* planes, const float* alpha, const float* x, long long x_rows, float* y,
+                               long long m, long long n, int b, int beta, cudaStream_t stream);
+cudaError_t launch_bandwidth_probe(const uint32_t* words, long long m, long long n, const float* x, long long x_rows,
+                                   float* out, bool streaming, cudaStream_t stream);
+
 // Workspace for the fast path (bytes).
 size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b);
 // Grid planner: CTAs per 32-group block.
