@@ -186,7 +186,7 @@ def tile_keys(keys, n: int, mu: int, stream=None):
 
 
 def build_lut_block(x, group_begin: int, group_count: int, mu: int, layout: int = TableMajor,
-                    precision: str = "f32", stream=None):
+                    precision: str = "f32", stream=None, builder: int = _capi.LUT_DP):
     """build_lut_block on the GPU.  precision "f32": the fast path's
     bank-owned builder; "f64": the exact builder.  Returns (entries, ops)."""
     x = _cuda(x, torch.float32)
@@ -195,7 +195,7 @@ def build_lut_block(x, group_begin: int, group_count: int, mu: int, layout: int 
                           device=x.device)
     ops = C.c_uint64(0)
     fn = lib.bqg_build_lut_f32 if precision == "f32" else lib.bqg_build_lut_f64
-    check(fn(_ptr(x), x_rows, b, mu, group_begin, group_count, layout, _capi.LUT_DP, _ptr(entries), C.byref(ops),
+    check(fn(_ptr(x), x_rows, b, mu, group_begin, group_count, layout, builder, _ptr(entries), C.byref(ops),
              _stream(stream)))
     return entries, ops.value
 
