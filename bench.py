@@ -249,10 +249,13 @@ def run_ours(args):
         return e0.elapsed_time(e1)
 
     if args.profile:
-        # under ncu: W warm-up calls and one timed replay, nothing else
+        # under ncu: W warm-up calls, one timed replay, and a short single-call chain
         with torch.cuda.stream(stream):
             g_warm.replay()
             g_timed.replay()
+        g_chain = chain_graph(16)
+        with torch.cuda.stream(stream):
+            g_chain.replay()
         torch.cuda.synchronize()
         if rank == 0:
             print(json.dumps({"profile_run": True, "config": args.config, "steps": args.steps, "group": G}))
