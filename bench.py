@@ -164,6 +164,8 @@ def run_ours(args):
     import paper_2005_09904_b200.biqgemm as bq
 
     m, n, beta, b, mu = CONFIGS[args.config]
+    if args.batch:
+        b = args.batch  # batch sweep (C4: b = 1 .. 256)
     kb = key_bytes(m, n, beta, mu)  # per rank and call (weak scaling: each rank owns an m-row shard)
     dev = torch.device("cuda", local_rank)
     G = args.group
@@ -566,6 +568,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparators", action="store_true", help="skip the cuBLAS / unpack / probe reference points")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch b (C4 sweep)")
     ap.add_argument("--group", type=int, default=128, help="independent calls per grouped launch")
     ap.add_argument("--e2e-group", type=int, default=512, help="calls per bqg_layers_forward_host call (e2e leg)")
     ap.add_argument("--profile", action="store_true", help="for ncu: warm-up + one timed replay only, no JSON line")
