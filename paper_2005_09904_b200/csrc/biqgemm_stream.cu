@@ -429,6 +429,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     }
 
     // ---------------------------------------------------------- consumers
+    uint64_t pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     uint32_t rot[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -488,20 +490,21 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             }
             mbar_wait(&full[slot], kround & 1u);
             const uint32_t kbase = stage_addr(slot) + static_cast<uint32_t>(pos) * BETA * 1024u;
-            double sum;
-            switch (lb) {
-                case 0: sum = stream_unit<BETA, 0>(kbase, lane, rot, a); break;
-                case 1: sum = stream_unit<BETA, 128>(kbase, lane, rot, a); break;
-                case 2: sum = stream_unit<BETA, 0x10000>(kbase, lane, rot, a); break;
-                default: sum = stream_unit<BETA, 0x10080>(kbase, lane, rot, a); break;
-            }
+            // LUT buffer lb = half lb of the 64 KiB region (nlb = 2): +128 B
+            const double sum = lb == 0 ? stream_unit<BETA, 0>(kbase, lane, rot, a)
+                                       : stream_unit<BETA, 128>(kbase, lane, rot, a);
             __syncwarp();
             if (lane == 0) {
                 // the last unit of a partial (call-final) stage completes its count
                 const int nin = min(A.ups, U - sj * A.ups);
                 mbar_arrive_cnt(&empty[slot], pos == nin - 1 ? static_cast<uint32_t>(A.ups - nin + 1) : 1u);
             }
-            if (r < A.m) part[r] = static_cast<float>(sum);
+            if (r < A.m) {
+                // partials stay in L2 for the epilogue (the key stream is evict_first)
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(part + r), "f"(static_cast<float>(sum)),
+                             "l"(pol_keep)
+                             : "memory");
+            }
         }
         __syncwarp();
         if (lane == 0) {
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(256) stream_finalize_kernel(const __grid_const
     const long long MTP = static_cast<long long>(A.MT) * 32;
     const float* p = A.partial + static_cast<long long>(c) * A.NB * MTP + r;
     double s = 0.0;
-    for (int gb = 0; gb < A.NB; ++gb) s += static_cast<double>(__ldcg(p + gb * MTP));
+    for (int gb = 0; gb < A.NB; ++gb) s += static_cast<double>(__ldcs(p + gb * MTP));  // read once: evict first
     A.calls[c].y[r] = static_cast<float>(s);
 }
 
