@@ -636,6 +636,16 @@ struct bqg_layer {
     size_t x_cap = 0;
     float* d_y = nullptr;
     size_t y_cap = 0;
+    float* h_x_pin = nullptr;  // pinned staging for pageable caller buffers (forward_host)
+    size_t hx_cap = 0;
+    float* h_y_pin = nullptr;
+    size_t hy_cap = 0;
+    // cached CUDA graph of one host forward (H2D -> kernels -> D2H) for the
+    // last (x_rows, b, exact) shape; captured on the second call of a shape
+    cudaGraphExec_t gexec = nullptr;
+    size_t g_xrows = 0, g_b = 0;
+    int g_exact = -1, g_seen = 0;
+    unsigned buf_gen = 0, g_gen = 0;  // bumped whenever a buffer the graph uses is reallocated
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::mutex mu_lock;
 
@@ -655,6 +665,9 @@ void layer_free(bqg_layer* L) {
     cudaFree(L->d_ws_exact);
     cudaFree(L->d_x);
     cudaFree(L->d_y);
+    cudaFreeHost(L->h_x_pin);
+    cudaFreeHost(L->h_y_pin);
+    if (L->gexec) cudaGraphExecDestroy(L->gexec);
     for (auto& e : L->ev)
         if (e) cudaEventDestroy(e);
     if (L->stream) cudaStreamDestroy(L->stream);
@@ -855,6 +868,7 @@ int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float
                   cudaStream_t st) {
     if (exact || L->mu > 8) {
         const size_t need = bqg_biqgemm_exact_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
+        if (need > L->ws_exact_bytes) ++L->buf_gen;
         int s = grow(L->d_ws_exact, L->ws_exact_bytes, need);
         if (s) return s;
         return bqg_biqgemm_exact_f32(L->d_keys, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu,
@@ -862,6 +876,7 @@ int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float
     }
     const size_t need = bqg_biqgemm_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
     if (need > L->ws_bytes) {
+        ++L->buf_gen;
         int s = grow(L->d_ws, L->ws_bytes, need);
         if (s) return s;
     }
@@ -880,26 +895,115 @@ extern "C" int bqg_layer_forward_device(bqg_layer* L, const float* d_x, size_t x
     return layer_forward(L, d_x, x_rows, b, d_y, exact, pdl, as_stream(stream));
 }
 
+namespace {
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+template <typename P>
+int grow_host(P*& ptr, size_t& cap, size_t need) {
+    if (need <= cap) return BQG_OK;
+    cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
+    BQG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ptr), need, cudaHostAllocDefault));
+    cap = need;
+    return BQG_OK;
+}
+}  // namespace
+
 extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_rows, size_t b, float* h_y,
                                       int exact, bqg_kernel_stats* stats) {
     if (!L || !h_x || !h_y) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null argument");
     int s = check_x(x_rows, b, L->n, L->mu, "biqgemm");
     if (s) return s;
     std::lock_guard<std::mutex> g(L->mu_lock);
-    s = grow(L->d_x, L->x_cap, sizeof(float) * x_rows * b);
+    const size_t xbytes = sizeof(float) * x_rows * b, ybytes = sizeof(float) * L->m * b;
+    if (xbytes > L->x_cap || ybytes > L->y_cap || xbytes > L->hx_cap || ybytes > L->hy_cap) ++L->buf_gen;
+    s = grow(L->d_x, L->x_cap, xbytes);
     if (s) return s;
-    s = grow(L->d_y, L->y_cap, sizeof(float) * L->m * b);
+    s = grow(L->d_y, L->y_cap, ybytes);
     if (s) return s;
+    // Steady state (no stats requested): the caller's x is copied into the
+    // layer's pinned staging, one cached CUDA graph runs H2D -> kernels ->
+    // D2H, and y is copied out -- one API launch per call instead of five.
+    if (!stats) {
+        const bool same = L->g_xrows == x_rows && L->g_b == b && L->g_exact == exact && L->g_gen == L->buf_gen;
+        if (!same) {
+            if (L->gexec) cudaGraphExecDestroy(L->gexec);
+            L->gexec = nullptr;
+            L->g_xrows = x_rows;
+            L->g_b = b;
+            L->g_exact = exact;
+            L->g_gen = L->buf_gen;
+            L->g_seen = 0;
+        }
+        s = grow_host(L->h_x_pin, L->hx_cap, xbytes);
+        if (s) return s;
+        s = grow_host(L->h_y_pin, L->hy_cap, ybytes);
+        if (s) return s;
+        std::memcpy(L->h_x_pin, h_x, xbytes);
+        cudaStream_t st = L->stream;
+        if (!L->gexec && L->g_seen >= 1) {  // second call of this shape: capture
+            cudaGraph_t graph = nullptr;
+            BQG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = cudaMemcpyAsync(L->d_x, L->h_x_pin, xbytes, cudaMemcpyHostToDevice, st);
+            int fs = e == cudaSuccess ? layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st) : BQG_OK;
+            if (e == cudaSuccess && fs == BQG_OK)
+                e = cudaMemcpyAsync(L->h_y_pin, L->d_y, ybytes, cudaMemcpyDeviceToHost, st);
+            cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+            if (fs) {
+                if (graph) cudaGraphDestroy(graph);
+                return fs;
+            }
+            if (e != cudaSuccess || e2 != cudaSuccess) {
+                if (graph) cudaGraphDestroy(graph);
+                return cuda_err(e != cudaSuccess ? e : e2, "forward graph capture");
+            }
+            e = cudaGraphInstantiate(&L->gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) return cuda_err(e, "forward graph instantiate");
+        }
+        if (L->gexec) {
+            BQG_CUDA(cudaGraphLaunch(L->gexec, st));
+        } else {
+            BQG_CUDA(cudaMemcpyAsync(L->d_x, L->h_x_pin, xbytes, cudaMemcpyHostToDevice, st));
+            s = layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st);
+            if (s) return s;
+            BQG_CUDA(cudaMemcpyAsync(L->h_y_pin, L->d_y, ybytes, cudaMemcpyDeviceToHost, st));
+            ++L->g_seen;
+        }
+        BQG_CUDA(cudaStreamSynchronize(st));
+        std::memcpy(h_y, L->h_y_pin, ybytes);
+        return BQG_OK;
+    }
+    // With stats: the same work step by step, event-timed.  Pageable caller
+    // buffers are staged through the layer's pinned buffers.
+    const bool xpin = is_pinned(h_x), ypin = is_pinned(h_y);
+    if (!xpin) {
+        s = grow_host(L->h_x_pin, L->hx_cap, xbytes);
+        if (s) return s;
+        std::memcpy(L->h_x_pin, h_x, xbytes);
+    }
+    if (!ypin) {
+        s = grow_host(L->h_y_pin, L->hy_cap, ybytes);
+        if (s) return s;
+    }
     cudaStream_t st = L->stream;
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[0], st));
-    BQG_CUDA(cudaMemcpyAsync(L->d_x, h_x, sizeof(float) * x_rows * b, cudaMemcpyHostToDevice, st));
+    BQG_CUDA(cudaMemcpyAsync(L->d_x, xpin ? h_x : L->h_x_pin, xbytes, cudaMemcpyHostToDevice, st));
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[1], st));
     s = layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st);
     if (s) return s;
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[2], st));
-    BQG_CUDA(cudaMemcpyAsync(h_y, L->d_y, sizeof(float) * L->m * b, cudaMemcpyDeviceToHost, st));
+    BQG_CUDA(cudaMemcpyAsync(ypin ? h_y : L->h_y_pin, L->d_y, ybytes, cudaMemcpyDeviceToHost, st));
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[3], st));
     BQG_CUDA(cudaStreamSynchronize(st));
+    if (!ypin) std::memcpy(h_y, L->h_y_pin, ybytes);
     if (stats) {
         uint64_t ops[4];
         bqg_op_counters(L->m, L->n, b, L->beta, L->mu, BQG_LUT_DP, ops);

@@ -178,3 +178,35 @@ def test_single_call_latency_form_matches_stream_form(bq, port, cuda, m, n, beta
     torch.cuda.synchronize()
     y_ref2, _ = port.biqgemm(keys.astype(np.uint32), None, n, 8, xs.cpu().numpy())
     assert_close(y_t.cpu().numpy(), y_ref2)
+
+
+def test_host_forward_graph_cache_survives_buffer_regrowth(bq, port, cuda):
+    """bqg_layer_forward_host caches a CUDA graph per shape (H2D -> kernels ->
+    D2H); new x each call, other shapes and entry points that regrow the
+    layer's buffers in between must not break it."""
+    import torch
+
+    m, n = 300, 1000
+    layer = bq.PackedLinear.from_weights(bq.random_uniform(m, n, 12), 3, 8)
+    keys, alpha = layer.export()
+    for i in range(6):  # captured on the 2nd-3rd call, replayed after
+        x = bq.random_normal(n, 1, 100 + i)
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x)
+        assert_close(layer.forward(x), y_ref)
+        if i == 3:  # a device forward with a larger b regrows the workspace
+            xb = torch.from_numpy(bq.random_normal(n, 7, 5)).cuda()
+            yb = torch.empty((m, 7), device="cuda")
+            layer.forward_device(xb, yb)
+            torch.cuda.synchronize()
+            y7, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, xb.cpu().numpy())
+            assert_close(yb.cpu().numpy(), y7)
+        if i == 4:  # another host shape in between
+            x2 = bq.random_normal(n, 2, 7)
+            y2, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x2)
+            assert_close(layer.forward(x2), y2)
+    x = bq.random_normal(n, 1, 999)
+    y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x)
+    for _ in range(3):
+        assert_close(layer.forward(x), y_ref)
+    assert np.array_equal(layer.forward(x, exact=True), layer.forward(x, exact=True))
+    layer.close()
