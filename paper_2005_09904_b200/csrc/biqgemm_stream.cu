@@ -279,17 +279,17 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMaxStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], A.ups);
+            mbar_init(&empty[s], A.ups * 32);  // every lane of a unit's warp arrives
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(&xfull[b], 32);
-            mbar_init(&xempty[b], kNBuild);
-            mbar_init(&lfull[b], kNBuild);
-            mbar_init(&ldone[b], kNC);
+            mbar_init(&xempty[b], kNBuild * 32);
+            mbar_init(&lfull[b], kNBuild * 32);
+            mbar_init(&ldone[b], kNC * 32);
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(&afull[b], 32);
-            mbar_init(&adone[b], kNC);
+            mbar_init(&adone[b], kNC * 32);
         }
         for (int s = 0; s < kMaxStages; ++s) issued[s] = 0;
         fence_mbar_init();
@@ -323,9 +323,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
                     "[%0], [%1], %2, [%3], %4;" ::"r"(stage_addr(slot)),
                     "l"(A.calls[c].keys + (u0 + k0) * BETA * 1024), "r"(bytes), "r"(smem_u32(&full[slot])), "l"(pol)
                     : "memory");
-                asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&issued[slot])),
-                             "r"(static_cast<uint32_t>(round + 1))
-                             : "memory");
+                // issued[slot] = round + 1 (one increment per round), as an atomic
+                asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&issued[slot])) : "memory");
             }
         }
         return;
@@ -419,11 +418,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             build_tables<kNBuild>(which, lut_abs + static_cast<uint32_t>(lb >> 1) * 0x10000u + static_cast<uint32_t>(lb & 1) * 128u +
                                     static_cast<uint32_t>(lane) * 4u,
                          xs + xb * kXBlock, lane);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&xempty[xb]);
-                mbar_arrive(&lfull[lb]);
-            }
+            // every lane releases its own table stores / x reads
+            mbar_arrive(&xempty[xb]);
+            mbar_arrive(&lfull[lb]);
         }
         return;
     }
@@ -493,9 +490,9 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
             // LUT buffer lb = half lb of the 64 KiB region (nlb = 2): +128 B
             const double sum = lb == 0 ? stream_unit<BETA, 0>(kbase, lane, rot, a)
                                        : stream_unit<BETA, 128>(kbase, lane, rot, a);
-            __syncwarp();
-            if (lane == 0) {
-                // the last unit of a partial (call-final) stage completes its count
+            {
+                // every lane releases its key reads; the last unit of a
+                // partial (call-final) stage completes the stage's count
                 const int nin = min(A.ups, U - sj * A.ups);
                 mbar_arrive_cnt(&empty[slot], pos == nin - 1 ? static_cast<uint32_t>(A.ups - nin + 1) : 1u);
             }
@@ -506,11 +503,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
                              : "memory");
             }
         }
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&ldone[lb]);
-            mbar_arrive(&adone[ab_i]);
-        }
+        mbar_arrive(&ldone[lb]);  // every lane: its LUT and alpha reads of call c are done
+        mbar_arrive(&adone[ab_i]);
     }
 }
 

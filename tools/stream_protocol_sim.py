@@ -92,7 +92,7 @@ def make(ncalls, U, ups, nst, nc, nlb, nab=2, nbuild=4):
                 yield ("atleast", ("issued", st % nst), st // nst + 1)
                 yield ("wait", ("full", st % nst), (st // nst) & 1, st // nst)
                 nin = min(ups, U - sj * ups)
-                yield ("arrive", ("empty", st % nst), ups - nin + 1 if pos == nin - 1 else 1)
+                yield ("arrive", ("empty", st % nst), ups - nin + 1 if pos == nin - 1 else 1)  # x32 lanes in the kernel
                 gu += nc
             yield ("arrive", ("ldone", c % nlb), 1)
             yield ("arrive", ("adone", c % nab), 1)
