@@ -342,7 +342,7 @@ def run_ours(args):
     GE = args.e2e_group  # calls per synchronised API call (the library pipelines copies inside it)
     x_pin = torch.from_numpy(np.stack([x_h[i % copies] for i in range(GE)])).pin_memory()
     y_pin = torch.empty((GE, m, b), dtype=torch.float32).pin_memory()
-    groups = [[e2e_layers[(st + i) % copies] for i in range(min(GE, args.steps - st))]
+    groups = [bq.LayerGroup([e2e_layers[(st + i) % copies] for i in range(min(GE, args.steps - st))])
               for st in range(0, args.steps, GE)]
     for grp in groups[:2]:
         bq.layers_forward_into(grp, x_pin[:len(grp)], y_pin[:len(grp)])

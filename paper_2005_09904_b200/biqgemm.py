@@ -369,12 +369,31 @@ class PackedLinear:
         return y
 
 
+class LayerGroup:
+    """A fixed sequence of layers for repeated layers_forward calls: the
+    handle array the C ABI takes is built once (building it from a Python
+    list costs ~0.15 us per layer on every call)."""
+
+    def __init__(self, layers):
+        self.layers = list(layers)  # keeps the layers alive
+        self._arr = (C.c_void_p * len(self.layers))(*[L._h.value for L in self.layers])
+
+    def __len__(self):
+        return len(self.layers)
+
+
 def layers_forward_into(layers, x, y, exact: bool = False, stats: KernelStats | None = None):
     """One biqgemm call per layer (layers share (m, n, beta, mu)) with HOST
     buffers: x is [count, x_rows, b], y is [count, m, b] (numpy or pinned
-    torch CPU tensors).  One H2D, the grouped kernels, one D2H, synchronised."""
+    torch CPU tensors).  The library pipelines H2D, the grouped kernels and
+    D2H in sub-groups, synchronised.  `layers` is a list or a LayerGroup."""
     count, x_rows, b = x.shape
-    arr = (C.c_void_p * count)(*[L._h.value for L in layers])
+    if isinstance(layers, LayerGroup):
+        if len(layers) != count:
+            raise ValueError(f"layers_forward: {len(layers)} layers for {count} inputs")
+        arr = layers._arr
+    else:
+        arr = (C.c_void_p * count)(*[L._h.value for L in layers])
     check(lib.bqg_layers_forward_host(C.cast(arr, C.c_void_p), count, _ptr(x), x_rows, b, _ptr(y),
                                       1 if exact else 0, C.byref(stats) if stats is not None else None))
     return y
@@ -382,7 +401,7 @@ def layers_forward_into(layers, x, y, exact: bool = False, stats: KernelStats | 
 
 def layers_forward(layers, x: np.ndarray, exact: bool = False, stats: KernelStats | None = None) -> np.ndarray:
     x = np.ascontiguousarray(x, np.float32)
-    m = layers[0].m
+    m = (layers.layers if isinstance(layers, LayerGroup) else layers)[0].m
     y = np.empty((x.shape[0], m, x.shape[2]), np.float32)
     return layers_forward_into(layers, x, y, exact, stats)
 

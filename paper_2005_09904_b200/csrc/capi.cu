@@ -1025,14 +1025,13 @@ namespace {
 // Process-wide per-device context for grouped host calls: a stream, event
 // pairs and grown-on-demand staging/workspace buffers, so a group's call does
 // not depend on which layer comes first.
-constexpr int kChunkEv = 8;
 struct GroupContext {
     std::mutex lock;
     cudaStream_t stream = nullptr;  // kernels
     cudaStream_t copy = nullptr;    // H2D
     cudaStream_t down = nullptr;    // D2H
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t chunk_ev[kChunkEv] = {};
+    std::vector<cudaEvent_t> chunk_ev;  // 2 per sub-group (H2D landed, kernels done), grown on demand
     float* d_x = nullptr;
     size_t x_cap = 0;
     float* d_y = nullptr;
@@ -1075,18 +1074,49 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
         BQG_CUDA(cudaStreamCreateWithFlags(&G.copy, cudaStreamNonBlocking));
         BQG_CUDA(cudaStreamCreateWithFlags(&G.down, cudaStreamNonBlocking));
         for (auto& e : G.ev) BQG_CUDA(cudaEventCreate(&e));
-        for (auto& e : G.chunk_ev) BQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     const size_t xs = x_rows * b, ys = L0->m * b;
     s = grow(G.d_x, G.x_cap, sizeof(float) * xs * count);
     if (s) return s;
     s = grow(G.d_y, G.y_cap, sizeof(float) * ys * count);
     if (s) return s;
-    // Pipelined in sub-groups of kSub calls: the H2D of sub-group k+1 (copy
-    // stream) and the D2H of sub-group k-1 (down stream) overlap the kernels
-    // of sub-group k (compute stream).  y is the same as one grouped call.
-    constexpr size_t kSub = 64;
-    const size_t nsub = (count + kSub - 1) / kSub;
+    // Pipelined in sub-groups: the H2D of sub-group k+1 (copy stream) and the
+    // D2H of sub-group k-1 (down stream) overlap the kernels of sub-group k
+    // (compute stream); consecutive grouped launches are PDL-chained.  The
+    // sub-groups ramp up (32, 64: each H2D lands while the previous,
+    // half-size sub-group computes) to kSub calls (grouped-launch efficiency)
+    // and ramp down at the end (64, 32: the last D2H is short).  y is the
+    // same as one grouped call.
+    static size_t kFirst = 0, kSub = 0;
+    if (kSub == 0) {
+        const char* e1 = getenv("BQG_E2E_FIRST");
+        const char* e2 = getenv("BQG_E2E_SUB");
+        kFirst = e1 ? std::max<size_t>(1, strtoull(e1, nullptr, 10)) : 32;
+        kSub = e2 ? std::max<size_t>(1, strtoull(e2, nullptr, 10)) : 128;
+    }
+    std::vector<size_t> starts{0};
+    {
+        size_t rem = count;
+        auto take = [&](size_t c) {
+            c = std::min(c, rem);
+            if (c) starts.push_back(starts.back() + c), rem -= c;
+        };
+        for (size_t sz = kFirst; sz < kSub && rem; sz *= 2) take(sz);
+        std::vector<size_t> down;
+        size_t dsum = 0;
+        for (size_t sz = kFirst; sz < kSub; sz *= 2) down.push_back(sz), dsum += sz;
+        if (rem >= dsum + kSub) {
+            while (rem > dsum) take(std::min(kSub, rem - dsum));
+            for (auto it = down.rbegin(); it != down.rend(); ++it) take(*it);
+        }
+        while (rem) take(kSub);
+    }
+    const size_t nsub = starts.size() - 1;
+    while (G.chunk_ev.size() < 2 * nsub) {
+        cudaEvent_t e;
+        BQG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        G.chunk_ev.push_back(e);
+    }
     s = grow(G.d_ws, G.ws_cap,
              bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, std::min(count, kSub)));
     if (s) return s;
@@ -1094,15 +1124,19 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
     for (size_t i = 0; i < count; ++i) calls[i] = {layers[i]->d_tiled, layers[i]->d_alpha, G.d_x + i * xs, G.d_y + i * ys};
     cudaStream_t st = G.stream, cp = G.copy, dp = G.down;
     if (stats) BQG_CUDA(cudaEventRecord(G.ev[0], cp));
+    // all H2D copies are queued first (the copy stream runs ahead of the kernels)
     for (size_t k = 0; k < nsub; ++k) {
-        const size_t i0 = k * kSub, cnt = std::min(kSub, count - i0);
-        cudaEvent_t h2d = G.chunk_ev[(2 * k) % kChunkEv], done = G.chunk_ev[(2 * k + 1) % kChunkEv];
+        const size_t i0 = starts[k], cnt = starts[k + 1] - i0;
         BQG_CUDA(cudaMemcpyAsync(G.d_x + i0 * xs, h_x + i0 * xs, sizeof(float) * xs * cnt, cudaMemcpyHostToDevice, cp));
-        BQG_CUDA(cudaEventRecord(h2d, cp));
+        BQG_CUDA(cudaEventRecord(G.chunk_ev[2 * k], cp));
+    }
+    for (size_t k = 0; k < nsub; ++k) {
+        const size_t i0 = starts[k], cnt = starts[k + 1] - i0;
+        cudaEvent_t h2d = G.chunk_ev[2 * k], done = G.chunk_ev[2 * k + 1];
         BQG_CUDA(cudaStreamWaitEvent(st, h2d, 0));
         if (stats && k == 0) BQG_CUDA(cudaEventRecord(G.ev[1], st));
-        s = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap, 0,
-                                    st);
+        s = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap,
+                                    k > 0 ? 1 : 0, st);
         if (s) return s;
         BQG_CUDA(cudaEventRecord(done, st));
         BQG_CUDA(cudaStreamWaitEvent(dp, done, 0));

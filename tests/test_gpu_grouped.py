@@ -149,6 +149,31 @@ def test_layers_forward_host(bq, port, cuda):
         L.close()
 
 
+def test_layers_forward_host_pipeline(bq, port, cuda):
+    """Many calls in one host call: the library's sub-group pipeline (ramp up,
+    128-call sub-groups, ramp down) gives every call its own result; a
+    LayerGroup is the same call as a list, bitwise."""
+    m, n, beta, count = 96, 512, 2, 300
+    base = [bq.PackedLinear.from_weights(bq.random_uniform(m, n, 500 + i), beta, 8) for i in range(3)]
+    layers = [base[i % 3] for i in range(count)]
+    x = np.stack([bq.random_normal(n, 1, 700 + i) for i in range(count)])
+    y = bq.layers_forward(layers, x)
+    y2 = bq.layers_forward(bq.LayerGroup(layers), x)
+    assert np.array_equal(y, y2)
+    # every call against the reference port (spot-check across sub-group seams)
+    for i in (0, 31, 32, 95, 96, 150, 203, 204, 235, 236, 267, 268, 299):
+        keys, alpha = layers[i].export()
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x[i])
+        assert_close(y[i], y_ref)
+    # and a sub-group boundary does not change any call's bits
+    y3 = bq.layers_forward(layers[:150], x[:150])
+    assert np.array_equal(y3, y[:150])
+    with pytest.raises(ValueError):
+        bq.layers_forward_into(bq.LayerGroup(layers[:5]), x[:4], np.empty((4, m, 1), np.float32))
+    for L in base:
+        L.close()
+
+
 @pytest.mark.parametrize("m,n,beta", [(1, 8, 1), (33, 7, 2), (100, 300, 3), (1000, 777, 4), (4096, 4096, 3),
                                       (2000, 4096, 1), (16384, 4096, 3), (70, 2048, 2), (5000, 1024, 3)])
 def test_single_call_latency_form_matches_stream_form(bq, port, cuda, m, n, beta):
