@@ -177,11 +177,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
                 const uint32_t w[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
                 float o[BT];
                 gather_chunk<MU, BT>(w, lut_s, goff, o);
-                float* dst = p.partial + ((static_cast<long long>(ii) * p.NB + gb) * rows_pad + ti * 32 + lane) * p.b +
-                             static_cast<long long>(ct) * BT;
-#pragma unroll
-                for (int cc = 0; cc < BT; ++cc)
-                    if (ct * BT + cc < p.b) dst[cc] = o[cc];
+                // partial[i*NB + gb][ct][row][BT]: the warp's 32 rows x BT
+                // columns are one contiguous 128*BT-byte run (one vector
+                // store per lane; padding columns past b are written and
+                // never read)
+                float* dst = p.partial +
+                             (((static_cast<long long>(ii) * p.NB + gb) * plan.CT + ct) * rows_pad + ti * 32 + lane) * BT;
+                if constexpr (BT == 4) {
+                    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+                } else if constexpr (BT == 2) {
+                    *reinterpret_cast<float2*>(dst) = make_float2(o[0], o[1]);
+                } else {
+                    dst[0] = o[0];
+                }
             }
             ti += dq;
             ii += dr;
@@ -201,28 +209,51 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
 }
 
 // y(r, c) = sum_i alpha_i[r] * (sum_gb partial[i][gb][r][c]), fp64, ascending
-// planes and group blocks (kernel.hpp:183-195).  One thread per output;
-// loads issued 16 at a time.
+// planes and group blocks (kernel.hpp:183-195).  One thread per output,
+// threads ordered (column tile, row, column in tile) so that every partial
+// load of a warp is one contiguous run; loads issued 16 at a time.
 __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
     pdl_launch_dependents();
     pdl_wait();
-    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= static_cast<long long>(p.m) * p.b) return;
-    const long long r = idx / p.b;
+    // 32-bit index math (m * b_pad < 2^32; BT is 1, 2 or 4)
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int BT = p.bt;
+    const int lg = BT == 4 ? 2 : (BT == 2 ? 1 : 0);
+    const uint32_t CT = static_cast<uint32_t>((p.b + BT - 1) / BT);
+    const uint32_t cc = tid & static_cast<uint32_t>(BT - 1), rt = tid >> lg;
+    const uint32_t ct = rt / static_cast<uint32_t>(p.m);
+    const long long r = rt - ct * static_cast<uint32_t>(p.m);
+    const long long col = static_cast<long long>(ct) * BT + cc;
+    if (ct >= CT || col >= p.b) return;
+    const long long idx = r * p.b + col;  // output element
     const long long rows_pad = static_cast<long long>(p.MT) * 32;
     const int total = p.NB * p.beta;  // q = i*NB + gb
-    const long long stride = rows_pad * p.b;
-    const float* src = p.partial + idx;  // row r, column c of partial q = 0
+    const long long stride = static_cast<long long>(CT) * rows_pad * BT;
+    const float* src = p.partial + (static_cast<long long>(ct) * rows_pad + r) * BT + cc;  // partial q = 0
+    // every load is issued ahead of its use: the plane scales up front, and
+    // the partials in batches of 32 with the next batch in flight while the
+    // current one is summed (the finaliser is latency-bound otherwise)
+    constexpr int KB = 32, KA = 8;
+    float a[KA];
+#pragma unroll
+    for (int t = 0; t < KA; ++t)
+        a[t] = (p.alpha && t < p.beta) ? __ldg(p.alpha + static_cast<long long>(t) * p.m + r) : 1.0f;
+    float v[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) v[k] = __ldcg(src + min(k, total - 1) * stride);
     double y = 0.0, acc = 0.0;
     int g = 0, i = 0;
-    double a_i = p.alpha ? static_cast<double>(__ldg(p.alpha + r)) : 1.0;
+    double a_i = static_cast<double>(a[0]);
 #pragma unroll 1
-    for (int q0 = 0; q0 < total; q0 += 16) {
-        float v[16];
+    for (int q0 = 0; q0 < total; q0 += KB) {
+        const bool more = q0 + KB < total;
+        float nv[KB];
+        if (more) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = __ldcg(src + min(q0 + k, total - 1) * stride);
+            for (int k = 0; k < KB; ++k) nv[k] = __ldcg(src + min(q0 + KB + k, total - 1) * stride);
+        }
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < KB; ++k) {
             if (q0 + k < total) {
                 acc += static_cast<double>(v[k]);
                 if (++g == p.NB) {
@@ -230,16 +261,29 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
                     acc = 0.0;
                     g = 0;
                     ++i;
-                    if (i < p.beta && p.alpha)
-                        a_i = static_cast<double>(__ldg(p.alpha + static_cast<long long>(i) * p.m + r));
+                    if (i < p.beta) {
+                        float an = 1.0f;
+#pragma unroll
+                        for (int t = 1; t < KA; ++t)
+                            if (t == i) an = a[t];
+                        if (i >= KA && p.alpha) an = __ldg(p.alpha + static_cast<long long>(i) * p.m + r);
+                        a_i = static_cast<double>(an);
+                    }
                 }
             }
+        }
+        if (more) {
+#pragma unroll
+            for (int k = 0; k < KB; ++k) v[k] = nv[k];
         }
     }
     p.y[idx] = static_cast<float>(y);
 }
 
-constexpr int kNW = 8;
+#ifndef BQG_FAST_NW
+#define BQG_FAST_NW 8
+#endif
+constexpr int kNW = BQG_FAST_NW;
 
 template <int BT>
 constexpr int stages_for() {
@@ -277,7 +321,7 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     if (e != cudaSuccess) return e;
     // finaliser: always PDL-chained to the fused kernel
     cudaLaunchConfig_t f = {};
-    const long long n = static_cast<long long>(p.m) * p.b;
+    const long long n = static_cast<long long>(p.m) * ((p.b + BT - 1) / BT) * BT;  // (column tile, row, column) threads
     f.gridDim = dim3(static_cast<unsigned>((n + 127) / 128));
     f.blockDim = dim3(128);
     f.stream = stream;
@@ -296,7 +340,14 @@ cudaError_t launch_mu(const QueryParams& p, const FastPlan& plan, int bt, bool p
     return launch_mu_bt<MU, 4>(p, plan, pdl, s);
 }
 
-int pick_bt(long long b) { return b == 1 ? 1 : (b == 2 ? 2 : 4); }
+int pick_bt(long long b) {
+    static const int force = [] {  // BQG_FAST_BT: experiment knob (1, 2 or 4)
+        const char* e = getenv("BQG_FAST_BT");
+        return e ? atoi(e) : 0;
+    }();
+    if (b > 1 && (force == 1 || force == 2 || force == 4)) return force;
+    return b == 1 ? 1 : (b == 2 ? 2 : 4);
+}
 
 FastPlan make_plan(long long m, long long groups, int beta, long long b, int mu, int num_sms) {
     const int BT = pick_bt(b);
@@ -348,7 +399,8 @@ FastPlan make_plan(long long m, long long groups, int beta, long long b, int mu,
 
 size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b) {
     const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
-    return static_cast<size_t>(NB) * beta * MT * 32 * b * sizeof(float);
+    const long long BT = pick_bt(b), bpad = (b + BT - 1) / BT * BT;  // column tiles are written whole
+    return static_cast<size_t>(NB) * beta * MT * 32 * std::max(b, bpad) * sizeof(float);
 }
 
 int plan_cpb(long long m, long long groups, int beta, long long b, int num_sms) {
@@ -379,6 +431,7 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
     }
     QueryParams p = p_in;
     p.debug = debug_flags;
+    p.bt = pick_bt(p.b);
     // The single-kernel cluster form wins when the per-call fixed costs
     // dominate and one column tile covers b (measured: C2 6.6 vs 8.5 us); the
     // two-kernel form (148 CTAs, cost-model split) wins for larger b / m.

@@ -31,9 +31,10 @@ struct QueryParams {
     const float* alpha;     // beta x m or nullptr (plane mode: alpha = 1)
     const float* x;         // x_rows x b
     float* y;               // m x b
-    float* partial;         // beta x NB x (MT*32) x b   (workspace, plane-major)
+    float* partial;         // workspace: plane-major partial sums (layout per form)
     long long x_rows;
     int m, G, NB, MT, beta, b, cpb;
+    int bt;     // fast form: input columns per column tile (1, 2 or 4)
     int debug;  // profiling switches (BQG_DEBUG_FLAGS); 0 in production
 };
 
