@@ -209,45 +209,65 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
 }
 
 // y(r, c) = sum_i alpha_i[r] * (sum_gb partial[i][gb][r][c]), fp64, ascending
-// planes and group blocks (kernel.hpp:183-195).  One thread per output,
-// threads ordered (column tile, row, column in tile) so that every partial
-// load of a warp is one contiguous run; loads issued 16 at a time.
+// planes and group blocks (kernel.hpp:183-195).  One thread per (column
+// tile, row): the BT columns of a partial are one vector load, and every load
+// is issued ahead of its use -- the plane scales up front, the partials in
+// batches of KB vectors with the next batch in flight while the current one
+// is summed (the finaliser is latency-bound otherwise).
+template <int BT>
+struct VecT;
+template <>
+struct VecT<1> {
+    using T = float;
+    static __device__ __forceinline__ float get(const float& v, int) { return v; }
+};
+template <>
+struct VecT<2> {
+    using T = float2;
+    static __device__ __forceinline__ float get(const float2& v, int c) { return c == 0 ? v.x : v.y; }
+};
+template <>
+struct VecT<4> {
+    using T = float4;
+    static __device__ __forceinline__ float get(const float4& v, int c) {
+        return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+    }
+};
+
+// COLS = BT: a thread owns a whole column tile (vector loads); COLS = 1: one
+// column (scalar loads, BT times the threads -- for few output tiles).
+template <int BT, int COLS>
 __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
+    using V = typename VecT<COLS>::T;
     pdl_launch_dependents();
     pdl_wait();
-    // 32-bit index math (m * b_pad < 2^32; BT is 1, 2 or 4)
-    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int BT = p.bt;
-    const int lg = BT == 4 ? 2 : (BT == 2 ? 1 : 0);
-    const uint32_t CT = static_cast<uint32_t>((p.b + BT - 1) / BT);
-    const uint32_t cc = tid & static_cast<uint32_t>(BT - 1), rt = tid >> lg;
-    const uint32_t ct = rt / static_cast<uint32_t>(p.m);
-    const long long r = rt - ct * static_cast<uint32_t>(p.m);
-    const long long col = static_cast<long long>(ct) * BT + cc;
-    if (ct >= CT || col >= p.b) return;
-    const long long idx = r * p.b + col;  // output element
+    const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long CT = (p.b + BT - 1) / BT;
+    const long long cc = COLS == 1 ? tid % BT : 0, rt = COLS == 1 ? tid / BT : tid;
+    const long long r = rt % p.m, ct = rt / p.m;
+    if (ct >= CT || ct * BT + cc >= p.b) return;
     const long long rows_pad = static_cast<long long>(p.MT) * 32;
     const int total = p.NB * p.beta;  // q = i*NB + gb
-    const long long stride = static_cast<long long>(CT) * rows_pad * BT;
-    const float* src = p.partial + (static_cast<long long>(ct) * rows_pad + r) * BT + cc;  // partial q = 0
-    // every load is issued ahead of its use: the plane scales up front, and
-    // the partials in batches of 32 with the next batch in flight while the
-    // current one is summed (the finaliser is latency-bound otherwise)
-    constexpr int KB = 32, KA = 8;
+    const long long stride = CT * rows_pad * (BT / COLS);  // in V units
+    const V* src = reinterpret_cast<const V*>(p.partial) + (ct * rows_pad + r) * (BT / COLS) + cc;  // partial q = 0
+    constexpr int BTC = COLS;  // columns summed by this thread
+    constexpr int KB = COLS == 4 ? 8 : (COLS == 2 ? 16 : 32), KA = 8;
     float a[KA];
 #pragma unroll
     for (int t = 0; t < KA; ++t)
         a[t] = (p.alpha && t < p.beta) ? __ldg(p.alpha + static_cast<long long>(t) * p.m + r) : 1.0f;
-    float v[KB];
+    V v[KB];
 #pragma unroll
     for (int k = 0; k < KB; ++k) v[k] = __ldcg(src + min(k, total - 1) * stride);
-    double y = 0.0, acc = 0.0;
+    double y[BTC], acc[BTC];
+#pragma unroll
+    for (int c = 0; c < BTC; ++c) y[c] = acc[c] = 0.0;
     int g = 0, i = 0;
     double a_i = static_cast<double>(a[0]);
 #pragma unroll 1
     for (int q0 = 0; q0 < total; q0 += KB) {
         const bool more = q0 + KB < total;
-        float nv[KB];
+        V nv[KB];
         if (more) {
 #pragma unroll
             for (int k = 0; k < KB; ++k) nv[k] = __ldcg(src + min(q0 + KB + k, total - 1) * stride);
@@ -255,10 +275,14 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
             if (q0 + k < total) {
-                acc += static_cast<double>(v[k]);
+#pragma unroll
+                for (int c = 0; c < BTC; ++c) acc[c] += static_cast<double>(VecT<COLS>::get(v[k], c));
                 if (++g == p.NB) {
-                    y += a_i * acc;
-                    acc = 0.0;
+#pragma unroll
+                    for (int c = 0; c < BTC; ++c) {
+                        y[c] += a_i * acc[c];
+                        acc[c] = 0.0;
+                    }
                     g = 0;
                     ++i;
                     if (i < p.beta) {
@@ -277,7 +301,10 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
             for (int k = 0; k < KB; ++k) v[k] = nv[k];
         }
     }
-    p.y[idx] = static_cast<float>(y);
+    float* yr = p.y + r * p.b + ct * BT + cc;
+#pragma unroll
+    for (int c = 0; c < BTC; ++c)
+        if (ct * BT + cc + c < p.b) yr[c] = static_cast<float>(y[c]);
 }
 
 #ifndef BQG_FAST_NW
@@ -321,7 +348,11 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     if (e != cudaSuccess) return e;
     // finaliser: always PDL-chained to the fused kernel
     cudaLaunchConfig_t f = {};
-    const long long n = static_cast<long long>(p.m) * ((p.b + BT - 1) / BT) * BT;  // (column tile, row, column) threads
+    // one thread per (column tile, row), or per (column tile, row, column)
+    // when the tiles alone give fewer than 128 threads per SM (measured crossover)
+    const long long tiles = static_cast<long long>(p.m) * ((p.b + BT - 1) / BT);
+    const bool per_col = BT > 1 && tiles < 148LL * 128;
+    const long long n = per_col ? tiles * BT : tiles;
     f.gridDim = dim3(static_cast<unsigned>((n + 127) / 128));
     f.blockDim = dim3(128);
     f.stream = stream;
@@ -330,7 +361,7 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     fa[0].val.programmaticStreamSerializationAllowed = 1;
     f.attrs = fa;
     f.numAttrs = 1;
-    return cudaLaunchKernelEx(&f, finalize_kernel, p);
+    return per_col ? cudaLaunchKernelEx(&f, finalize_kernel<BT, 1>, p) : cudaLaunchKernelEx(&f, finalize_kernel<BT, BT>, p);
 }
 
 template <int MU>

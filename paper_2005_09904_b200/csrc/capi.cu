@@ -474,9 +474,6 @@ extern "C" int bqg_biqgemm_f32(const uint8_t* d_keys, const float* d_alpha, cons
         const unsigned long long chunks = ((groups_of(n, mu) + 31) / 32) * ((m + 31) / 32) * beta *
                                           ((b + 3) / 4 + 1);
         if (chunks > 0x7fffffffull) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: problem too large for one call");
-        // the finaliser indexes outputs (column tiles padded to 4) in 32 bits
-        if (static_cast<unsigned long long>(m) * ((b + 3) / 4 * 4) > 0xffffffffull)
-            return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: problem too large for one call");
     }
     if (!d_keys || !d_x || !d_y || !d_ws) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null pointer");
     if (ws_bytes < bqg_biqgemm_workspace_bytes(m, n, b, beta, mu))
