@@ -118,6 +118,29 @@ def main():
                     summary[cfg] = {"dram_bytes_per_launch": rd + wr, "calls_per_launch": calls,
                                     "algorithmic_bytes_per_launch": alg, "duration_us_ncu": dur / 1e3,
                                     "kernel": name[:100], "round": tag}
+        # b >= 2 forms: the two-kernel fast form (tools/fast_sweep.py under ncu)
+        fp = d / f"fast_{cfg}.ncu-rep"
+        if fp.exists():
+            G = (n + mu - 1) // mu
+            lds_alg = 4 * beta * m * G * b  # LUT bytes gathered
+            rows = [k for k in raw(fp) if "biqgemm_fast_kernel" in str(k.get("Kernel Name"))
+                    or "finalize_kernel" in str(k.get("Kernel Name"))]
+            if rows:
+                L += [f"## {cfg} (m={m} n={n} q={beta} mu={mu} b={b}): two-kernel fast form, one single call", "",
+                      "| kernel | us | LDS GB/s (algorithmic) | shared wavefronts | LSU data pipe % | issue % | DRAM rd / wr MB | regs / threads / grid |",
+                      "|---|---|---|---|---|---|---|---|"]
+                for k in rows:
+                    dur = k.get("gpu__time_duration.sum") or 1
+                    nm = str(k.get("Kernel Name")).split("(")[0][:60]
+                    lsu = k.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") or 0
+                    gbs = lds_alg / dur if "fast_kernel" in nm else 0
+                    L.append(f"| `{nm}` | {dur / 1e3:.2f} | {gbs:.0f} | {lsu / 1e6:.2f} M | "
+                             f"{k.get('l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed')} | "
+                             f"{k.get('smsp__issue_active.avg.pct_of_peak_sustained_active')} | "
+                             f"{(k.get('dram__bytes_read.sum') or 0) / 1e6:.1f} / {(k.get('dram__bytes_write.sum') or 0) / 1e6:.1f} | "
+                             f"{k.get('launch__registers_per_thread')} / {k.get('launch__block_size')} / {k.get('launch__grid_size')} |")
+                L += ["", f"LDS roofline (128 B/clk/SM x 148 SMs x 1.9 GHz = 36 TB/s): {lds_alg / 36e12 * 1e6:.1f} us "
+                      f"for {lds_alg / 1e6:.0f} MB of gathered LUT bytes.", ""]
         lp = d / f"launches_{cfg}.csv"
         if lp.exists():
             shutil.copy(lp, PROF / f"ncu_launches_{tag}_{cfg}.csv")
