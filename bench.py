@@ -455,7 +455,7 @@ def comparators(bq, layer, w, x_h, m, n, beta, b, mu, kb, dev, calls=200):
         ws_ = [w0] + [w0.clone() for _ in range(nc - 1)]
         xs_ = [xx.to(dt) for xx in x_d]
         ys_ = [torch.empty((m, b), device=dev, dtype=dt) for _ in range(nc)]
-        us = timeit([(lambda j=j: torch.matmul(ws_[j % nc], xs_[j % 4], out=ys_[j % nc])) for j in range(calls)])
+        us = timeit([(lambda j=j: torch.matmul(ws_[j % nc], xs_[j % len(xs_)], out=ys_[j % nc])) for j in range(calls)])
         wbytes = w0.numel() * w0.element_size()
         out[name] = {"us_per_call": round(us, 3), "weight_bytes": int(wbytes),
                      "weight_gbs": round(wbytes / (us * 1e-6) / 1e9, 1)}
@@ -466,7 +466,7 @@ def comparators(bq, layer, w, x_h, m, n, beta, b, mu, kb, dev, calls=200):
     al = torch.from_numpy(alpha).to(dev)
     yy = [torch.empty((m, b), device=dev) for _ in range(nc)]
     if b <= 8 and n * b * 4 <= 200 * 1024:
-        us = timeit([(lambda j=j: bq.gemm_unpack_device(ps[j % nc], al, x_d[j % 4], yy[j % nc], m, n, beta,
+        us = timeit([(lambda j=j: bq.gemm_unpack_device(ps[j % nc], al, x_d[j % len(x_d)], yy[j % nc], m, n, beta,
                                                         stream=torch.cuda.current_stream().cuda_stream))
                      for j in range(calls)])
         out["gemm_unpack_gpu"] = {"us_per_call": round(us, 3), "key_gbs": round(kb / (us * 1e-6) / 1e9, 1)}
