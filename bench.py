@@ -26,8 +26,9 @@ each PDL-chained behind its predecessor (consecutive layers of one model).
 
 e2e: the same calls through the public C ABI with HOST buffers
 (bqg_layers_forward_host per 512 calls: H2D of the inputs from pinned
-in sub-groups (32, 64, 128 ... 128, 64, 32 calls) on separate streams -- synchronised), wall-clock timed.
-in 64-call sub-groups on separate streams -- synchronised), wall-clock timed.
+memory, the grouped kernels, D2H of the outputs -- pipelined inside the call
+in sub-groups of 32, 64, 128 ... 128, 64, 32 calls on separate streams --
+synchronised), wall-clock timed.
 
 N>1 (torchrun): weak scaling -- every rank owns a C2-sized row shard of an
 (N*4096) x 4096 layer, and y is assembled with an NCCL all-gather each step.
