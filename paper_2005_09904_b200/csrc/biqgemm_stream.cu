@@ -509,6 +509,10 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
 }
 
 __global__ void __launch_bounds__(256) stream_finalize_kernel(const __grid_constant__ StreamArgs A) {
+    // the next grouped launch may start now: its key stream does not depend
+    // on us, and its x / partial accesses wait (griddepcontrol.wait) for this
+    // grid to complete
+    pdl_launch_dependents();
     pdl_wait();
     const int c = blockIdx.y;
     const long long r = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
