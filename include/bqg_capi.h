@@ -161,7 +161,9 @@ int bqg_biqgemm_f32(const uint8_t* d_keys_tiled, const float* d_alpha, const flo
 /* Which single-call kernel form bqg_biqgemm_f32 uses for this shape on the
  * current device: 1 = latency form (b == 1, mu == 8, beta <= 4, n <= 4096:
  * one kernel, in-cluster push reduction, y bitwise equal to the grouped
- * form), 2 = cluster form, 3 = two-kernel form; 0 = no fast path. */
+ * form), 2 = cluster form, 3 = two-kernel form, 4 = the grouped stream form
+ * with a group of one (b == 1, mu == 8, beta <= 4 shapes outside forms 1-2,
+ * e.g. large m; y bitwise equal to the grouped form); 0 = no fast path. */
 int bqg_biqgemm_form(size_t m, size_t n, size_t b, unsigned beta, unsigned mu);
 
 /* Grouped calls: `count` independent biqgemm calls (kernel.hpp:246-258, one

@@ -446,6 +446,7 @@ int fast_form(const QueryParams& p, int mu) {
     if (!(debug_flags & (128 | 8192 | 16384)) && latency_supported(mu, p.beta, p.b, p.NB) && latency_applies(p)) return 1;
     const bool cluster_shape = p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
     if (!(debug_flags & 128) && (cluster_shape || (debug_flags & 8192))) return 2;  // (if the device can co-schedule it)
+    if (!(debug_flags & (128 | 8192 | 65536)) && stream_supported(mu, p.beta, p.b)) return 4;
     return 3;
 }
 
@@ -476,6 +477,15 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
         bool used = false;
         cudaError_t e = launch_biqgemm_cluster(p, mu, pdl, stream, &used);
         if (e != cudaSuccess || used) return e;
+    }
+    // b == 1, mu == 8, beta <= 4 shapes outside the latency / cluster forms
+    // (large m, e.g. C4): the grouped stream form with a group of one beats
+    // the two-kernel form (C4: 12.4 vs 14.0 us per dependent call), and its
+    // y is bitwise the grouped form's.  The single-call workspace is larger
+    // than the stream form's (beta x the partials).
+    if (!(debug_flags & (128 | 8192 | 65536)) && stream_supported(mu, p.beta, p.b)) {
+        const StreamCall call{p.keys, p.alpha, p.x, p.y};
+        return launch_biqgemm_stream(&call, 1, p.x_rows, p.m, p.G, p.beta, p.partial, pdl, stream);
     }
     const FastPlan plan = make_plan(p.m, p.G, p.beta, p.b, mu, sms);
     const int bt = pick_bt(p.b);

@@ -58,7 +58,8 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
 bool latency_supported(int mu, int beta, long long b, int NB);
 cudaError_t launch_biqgemm_latency(const QueryParams& p, bool pdl, cudaStream_t stream, bool* used);
 bool latency_applies(const QueryParams& p);
-// Which single-call form launch_biqgemm_fast picks: 1 latency, 2 cluster, 3 two-kernel.
+// Which single-call form launch_biqgemm_fast picks: 1 latency, 2 cluster, 3 two-kernel,
+// 4 stream form with a group of one.
 int fast_form(const QueryParams& p, int mu);
 
 // Comparison baselines (baselines.cu; reference baselines.hpp:40-87).
