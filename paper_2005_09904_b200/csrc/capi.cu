@@ -1083,16 +1083,17 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
     // Pipelined in sub-groups: the H2D of sub-group k+1 (copy stream) and the
     // D2H of sub-group k-1 (down stream) overlap the kernels of sub-group k
     // (compute stream); consecutive grouped launches are PDL-chained.  The
-    // sub-groups ramp up (32, 64: each H2D lands while the previous,
-    // half-size sub-group computes) to kSub calls (grouped-launch efficiency)
-    // and ramp down at the end (64, 32: the last D2H is short).  y is the
-    // same as one grouped call.
+    // sub-groups ramp up (64, 128: each H2D lands while the previous,
+    // half-size sub-group computes) to kSub = 256 calls (grouped-launch
+    // efficiency) and ramp down at the end (128, 64: the last D2H is short)
+    // when there is room (measured best of 16/32/64 first x 128/256 sub-group
+    // sizes, C2 512 calls).  y is the same as one grouped call.
     static size_t kFirst = 0, kSub = 0;
     if (kSub == 0) {
         const char* e1 = getenv("BQG_E2E_FIRST");
         const char* e2 = getenv("BQG_E2E_SUB");
-        kFirst = e1 ? std::max<size_t>(1, strtoull(e1, nullptr, 10)) : 32;
-        kSub = e2 ? std::max<size_t>(1, strtoull(e2, nullptr, 10)) : 128;
+        kFirst = e1 ? std::max<size_t>(1, strtoull(e1, nullptr, 10)) : 64;
+        kSub = e2 ? std::max<size_t>(1, strtoull(e2, nullptr, 10)) : 256;
     }
     std::vector<size_t> starts{0};
     {

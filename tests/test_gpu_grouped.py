@@ -151,9 +151,9 @@ def test_layers_forward_host(bq, port, cuda):
 
 def test_layers_forward_host_pipeline(bq, port, cuda):
     """Many calls in one host call: the library's sub-group pipeline (ramp up,
-    128-call sub-groups, ramp down) gives every call its own result; a
+    256-call sub-groups, ramp down) gives every call its own result; a
     LayerGroup is the same call as a list, bitwise."""
-    m, n, beta, count = 96, 512, 2, 300
+    m, n, beta, count = 96, 512, 2, 700
     base = [bq.PackedLinear.from_weights(bq.random_uniform(m, n, 500 + i), beta, 8) for i in range(3)]
     layers = [base[i % 3] for i in range(count)]
     x = np.stack([bq.random_normal(n, 1, 700 + i) for i in range(count)])
@@ -161,7 +161,7 @@ def test_layers_forward_host_pipeline(bq, port, cuda):
     y2 = bq.layers_forward(bq.LayerGroup(layers), x)
     assert np.array_equal(y, y2)
     # every call against the reference port (spot-check across sub-group seams)
-    for i in (0, 31, 32, 95, 96, 150, 203, 204, 235, 236, 267, 268, 299):
+    for i in (0, 63, 64, 191, 192, 255, 256, 447, 448, 507, 508, 635, 636, 699):
         keys, alpha = layers[i].export()
         y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, 8, x[i])
         assert_close(y[i], y_ref)
