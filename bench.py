@@ -27,7 +27,7 @@ each PDL-chained behind its predecessor (consecutive layers of one model).
 e2e: the same calls through the public C ABI with HOST buffers
 (bqg_layers_forward_host per 512 calls: H2D of the inputs from pinned
 memory, the grouped kernels, D2H of the outputs -- pipelined inside the call
-in sub-groups of 64, 128, 256 ... 256, 128, 64 calls on separate streams --
+in sub-groups sized by host I/O (C2: 64, 128, 256 ... 128, 64 calls) --
 synchronised), wall-clock timed.
 
 N>1 (torchrun): weak scaling -- every rank owns a C2-sized row shard of an
@@ -397,7 +397,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(m * b * 4), "us_per_call": e2e_s / args.steps * 1e6,
                 "api": f"bqg_layers_forward_host, {GE} calls per synchronised API call "
                        "(H2D / grouped kernels / D2H pipelined inside the call in sub-groups ramping "
-                       "64-128-256..256-128-64 calls; LayerGroup handle array built once)"},
+                       "sized by host I/O, C2: 64-128-256..128-64 calls; LayerGroup handle array built once)"},
         "gpu_launches": 2 * n_launch if stream_form else args.steps * 2,
         "clocks": clocks,
         "parity_rel_fro": rel,

@@ -259,8 +259,8 @@ int bqg_layer_forward_host(bqg_layer* layer, const float* h_x, size_t x_rows, si
 /* biqgemm over a GROUP of layers that share (m, n, beta, mu) -- one call per
  * layer, each with its own x -- with HOST buffers: h_x is count x (x_rows x
  * b) contiguous, h_y is count x (m x b).  H2D of x, the grouped kernels
- * (bqg_biqgemm_grouped_f32) and D2H of y are pipelined in sub-groups of 64,
- * 128, 256 ... 256, 128, 64 calls on three streams (copies overlap kernels);
+ * (bqg_biqgemm_grouped_f32) and D2H of y are pipelined in sub-groups sized
+ * by host I/O (C2: 64, 128, 256 ... 128, 64 calls) on three streams;
  * synchronised before return.  Runs on a per-device library stream with its own staging and
  * workspace (thread-safe; calls are serialised).  exact != 0: the exact path per
  * layer.  stats (may be NULL) accumulates the counters of all calls. */

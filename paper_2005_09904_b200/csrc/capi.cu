@@ -1083,17 +1083,26 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
     // Pipelined in sub-groups: the H2D of sub-group k+1 (copy stream) and the
     // D2H of sub-group k-1 (down stream) overlap the kernels of sub-group k
     // (compute stream); consecutive grouped launches are PDL-chained.  The
-    // sub-groups ramp up (64, 128: each H2D lands while the previous,
-    // half-size sub-group computes) to kSub = 256 calls (grouped-launch
-    // efficiency) and ramp down at the end (128, 64: the last D2H is short)
-    // when there is room (measured best of 16/32/64 first x 128/256 sub-group
-    // sizes, C2 512 calls).  y is the same as one grouped call.
-    static size_t kFirst = 0, kSub = 0;
-    if (kSub == 0) {
-        const char* e1 = getenv("BQG_E2E_FIRST");
-        const char* e2 = getenv("BQG_E2E_SUB");
-        kFirst = e1 ? std::max<size_t>(1, strtoull(e1, nullptr, 10)) : 64;
-        kSub = e2 ? std::max<size_t>(1, strtoull(e2, nullptr, 10)) : 256;
+    // sub-groups ramp up (each H2D lands while the previous, half-size
+    // sub-group computes) to kSub calls (grouped-launch efficiency) and ramp
+    // down at the end (the last D2H is short) when there is room.  Sizes
+    // follow the calls' host I/O: the first sub-group moves ~2 MiB of x + y,
+    // the steady ones ~8 MiB (C2: 64 -> 128 -> 256 ... 256 -> 128 -> 64 calls,
+    // measured best of 16/32/64 x 128/256; a b = 256 call is its own
+    // sub-group).  y is the same as one grouped call.
+    size_t kFirst, kSub;
+    {
+        static const long long e_first = [] {
+            const char* e = getenv("BQG_E2E_FIRST");
+            return e ? atoll(e) : 0LL;
+        }();
+        static const long long e_sub = [] {
+            const char* e = getenv("BQG_E2E_SUB");
+            return e ? atoll(e) : 0LL;
+        }();
+        const size_t io = std::max<size_t>(1, sizeof(float) * (xs + ys));  // host bytes per call
+        kFirst = e_first > 0 ? static_cast<size_t>(e_first) : std::clamp<size_t>((2u << 20) / io, 1, 64);
+        kSub = e_sub > 0 ? static_cast<size_t>(e_sub) : std::clamp<size_t>((8u << 20) / io, 1, 256);
     }
     std::vector<size_t> starts{0};
     {
