@@ -234,8 +234,9 @@ struct VecT<4> {
     }
 };
 
-// COLS = BT: a thread owns a whole column tile (vector loads); COLS = 1: one
-// column (scalar loads, BT times the threads -- for few output tiles).
+// COLS = BT: a thread owns a whole column tile (vector loads); COLS = 2 or 1:
+// a slice of it (BT / COLS times the threads -- for fewer output tiles; the
+// launcher picks by tile count, measured crossovers).
 template <int BT, int COLS>
 __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
     using V = typename VecT<COLS>::T;
@@ -243,13 +244,14 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
     pdl_wait();
     const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long CT = (p.b + BT - 1) / BT;
-    const long long cc = COLS == 1 ? tid % BT : 0, rt = COLS == 1 ? tid / BT : tid;
+    constexpr int PER = BT / COLS;  // threads per column tile
+    const long long cc = tid % PER, rt = tid / PER;  // cc: which COLS-wide slice of the tile
     const long long r = rt % p.m, ct = rt / p.m;
-    if (ct >= CT || ct * BT + cc >= p.b) return;
+    if (ct >= CT || ct * BT + cc * COLS >= p.b) return;
     const long long rows_pad = static_cast<long long>(p.MT) * 32;
     const int total = p.NB * p.beta;  // q = i*NB + gb
-    const long long stride = CT * rows_pad * (BT / COLS);  // in V units
-    const V* src = reinterpret_cast<const V*>(p.partial) + (ct * rows_pad + r) * (BT / COLS) + cc;  // partial q = 0
+    const long long stride = CT * rows_pad * PER;  // in V units
+    const V* src = reinterpret_cast<const V*>(p.partial) + (ct * rows_pad + r) * PER + cc;  // partial q = 0
     constexpr int BTC = COLS;  // columns summed by this thread
     constexpr int KB = COLS == 4 ? 8 : (COLS == 2 ? 16 : 32), KA = 8;
     float a[KA];
@@ -301,10 +303,10 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
             for (int k = 0; k < KB; ++k) v[k] = nv[k];
         }
     }
-    float* yr = p.y + r * p.b + ct * BT + cc;
+    float* yr = p.y + r * p.b + ct * BT + cc * COLS;
 #pragma unroll
     for (int c = 0; c < BTC; ++c)
-        if (ct * BT + cc + c < p.b) yr[c] = static_cast<float>(y[c]);
+        if (ct * BT + cc * COLS + c < p.b) yr[c] = static_cast<float>(y[c]);
 }
 
 #ifndef BQG_FAST_NW
@@ -352,7 +354,8 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     // when the tiles alone give fewer than 128 threads per SM (measured crossover)
     const long long tiles = static_cast<long long>(p.m) * ((p.b + BT - 1) / BT);
     const bool per_col = BT > 1 && tiles < 148LL * 128;
-    const long long n = per_col ? tiles * BT : tiles;
+    const bool half = !per_col && BT == 4 && tiles < 148LL * 256;  // two threads per tile (float2)
+    const long long n = per_col ? tiles * BT : (half ? tiles * 2 : tiles);
     f.gridDim = dim3(static_cast<unsigned>((n + 127) / 128));
     f.blockDim = dim3(128);
     f.stream = stream;
@@ -361,7 +364,11 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     fa[0].val.programmaticStreamSerializationAllowed = 1;
     f.attrs = fa;
     f.numAttrs = 1;
-    return per_col ? cudaLaunchKernelEx(&f, finalize_kernel<BT, 1>, p) : cudaLaunchKernelEx(&f, finalize_kernel<BT, BT>, p);
+    if (per_col) return cudaLaunchKernelEx(&f, finalize_kernel<BT, 1>, p);
+    if constexpr (BT == 4) {
+        if (half) return cudaLaunchKernelEx(&f, finalize_kernel<4, 2>, p);
+    }
+    return cudaLaunchKernelEx(&f, finalize_kernel<BT, BT>, p);
 }
 
 template <int MU>
