@@ -148,14 +148,37 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     pdl_wait();  // x (and the workspace) of the predecessor are visible from here on
     if (tl) g_timeline[blockIdx.x][1] = gtimer();
     int sc = 0;
+    // The x tile of a segment's (block, column tile) is loaded into registers
+    // one segment ahead (its global latency overlaps the previous segment's
+    // gather) and stored to shared memory at the segment boundary -- the
+    // values stage_x_tile would read.
+    constexpr int XT = 32 * MU * BT, XPT = (XT + NW * 32 - 1) / (NW * 32);
+    float xr[XPT];
+    auto load_x = [&](int pair) {
+        const long long gbx = pair / plan.CT, col0 = static_cast<long long>(pair - gbx * plan.CT) * BT;
+        const long long r0 = gbx * 32 * MU;
+#pragma unroll
+        for (int k = 0; k < XPT; ++k) {
+            const int idx = threadIdx.x + k * NW * 32;
+            const int rl = idx / BT, c = idx - (idx / BT) * BT;
+            const long long r = r0 + rl, col = col0 + c;
+            xr[k] = (idx < XT && r < p.x_rows && col < p.b) ? __ldcg(p.x + r * p.b + col) : 0.0f;
+        }
+    };
+    if (cbeg < cend) load_x(cbeg / plan.cpp);
     for (int seg = cbeg; seg < cend;) {
         const int pair = seg / plan.cpp;
         const int pbase = pair * plan.cpp;
         const int seg_end = min(cend, pbase + plan.cpp);
         const int gb = pair / plan.CT, ct = pair - gb * plan.CT;
         if (seg != cbeg) named_bar_sync(1, NW * 32);  // previous segment done with the LUT and x tile
-        stage_x_tile<MU, BT>(xs, p.x, p.x_rows, p.b, gb, static_cast<long long>(ct) * BT, threadIdx.x, NW * 32);
+#pragma unroll
+        for (int k = 0; k < XPT; ++k) {
+            const int idx = threadIdx.x + k * NW * 32;
+            if (idx < XT) xs[idx] = xr[k];
+        }
         named_bar_sync(1, NW * 32);
+        if (seg_end < cend) load_x(seg_end / plan.cpp);  // the next segment's x, in flight during this one
         build_bank_owned_tables_smem<MU, NW, BT, LutGeom<BT>::KROW>(lut, xs, warp, lane);
         named_bar_sync(1, NW * 32);
         if (tl) g_timeline[blockIdx.x][2] = gtimer();
