@@ -161,14 +161,36 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         }
         const int dq = NW / beta, dr = NW - (NW / beta) * beta;
         int sc = 0;
+        // x tile of segment sg+1 loaded into registers during segment sg (the
+        // values stage_x_tile would read), stored at the segment boundary
+        constexpr int XT = 32 * MU * BT, XPT = (XT + NW * 32 - 1) / (NW * 32);
+        float xr[XPT];
+        auto load_x = [&](int sgx) {
+            const int ctx = sgx / nblk;
+            const long long gbx = rank + (sgx - ctx * nblk) * cs, col0 = static_cast<long long>(ctx) * BT;
+            const long long r0 = gbx * 32 * MU;
+#pragma unroll
+            for (int k = 0; k < XPT; ++k) {
+                const int idx = threadIdx.x + k * NW * 32;
+                const int rl = idx / BT, c = idx - (idx / BT) * BT;
+                const long long r = r0 + rl, col = col0 + c;
+                xr[k] = (idx < XT && r < p.x_rows && col < p.b) ? __ldcg(p.x + r * p.b + col) : 0.0f;
+            }
+        };
+        if (nseg > 0) load_x(0);
         for (int sg = 0; sg < nseg; ++sg) {
             const int ct = sg / nblk;
             const int bi = sg - ct * nblk;
             const int gb = rank + bi * cs;
             const bool first = bi == 0;  // first group block of this rank for this column tile
             if (sg != 0) named_bar_sync(1, NW * 32);  // previous segment done with the LUT and x tile
-            stage_x_tile<MU, BT>(xs, p.x, p.x_rows, p.b, gb, static_cast<long long>(ct) * BT, threadIdx.x, NW * 32);
+#pragma unroll
+            for (int k = 0; k < XPT; ++k) {
+                const int idx = threadIdx.x + k * NW * 32;
+                if (idx < XT) xs[idx] = xr[k];
+            }
             named_bar_sync(1, NW * 32);
+            if (sg + 1 < nseg) load_x(sg + 1);
             build_bank_owned_tables_smem<MU, NW, BT, LutGeom<BT>::KROW>(lut, xs, warp, lane);
             named_bar_sync(1, NW * 32);
             if (tl && sg == 0) g_timeline_c[blockIdx.x][2] = gtimer_c();
