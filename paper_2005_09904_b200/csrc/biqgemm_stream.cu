@@ -42,6 +42,7 @@
 // independent of the grid, the group size and any 32-row-aligned row
 // sharding.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -560,11 +561,20 @@ bool stream_supported(int mu, int beta, long long b) { return mu == kMU && b == 
 size_t stream_workspace_bytes(long long m, long long groups, int count) {
     const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
     const long long per = static_cast<long long>(std::min(count, kStreamMaxGroup));
-    return static_cast<size_t>(per * NB * MT * 32) * sizeof(float);
+    return kTexCounterBytes + static_cast<size_t>(per * NB * MT * 32) * sizeof(float);
 }
 
 cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
                                   float* ws, bool pdl, cudaStream_t stream) {
+    static const int impl = [] {
+        const char* v = getenv("BQG_STREAM_IMPL");
+        return (v && v[0] == 't' && v[1] == 'm') ? 1 : 0;  // "tma": the TMA-ring form below
+    }();
+    // The texture form finalises in-kernel (the last CTA to finish a call sums
+    // its partials), which pays off over a group; a call or two alone keeps
+    // this TMA-ring form, whose finaliser is a separate wide kernel.
+    if (impl == 0 && count >= kTexMinGroup && tex_stream_applies(m, G, beta))
+        return launch_biqgemm_tex(calls, count, x_rows, m, G, beta, ws, pdl, stream);
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;

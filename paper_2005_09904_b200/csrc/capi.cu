@@ -735,6 +735,7 @@ int grow(P*& ptr, size_t& cap, size_t need) {
     ptr = nullptr;
     cap = 0;
     BQG_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), need));
+    BQG_CUDA(cudaMemset(ptr, 0, need));  // workspaces must start zero-filled (grouped counters)
     cap = need;
     return BQG_OK;
 }

@@ -47,10 +47,21 @@ struct StreamCall {
     float* y;             // m x 1
 };
 constexpr int kStreamMaxGroup = 512;  // calls per launch (kernel-parameter array, 16 KiB)
+// The grouped workspace starts with one completion counter per call of a
+// launch (zero between launches: the kernel resets what it uses), then the
+// partial sums.
+constexpr size_t kTexCounterBytes = kStreamMaxGroup * sizeof(unsigned);
 bool stream_supported(int mu, int beta, long long b);
 size_t stream_workspace_bytes(long long m, long long groups, int count);
 cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
                                   float* ws, bool pdl, cudaStream_t stream);
+// The same grouped computation with the keys fetched through the texture
+// pipe (biqgemm_tex.cu); launch_biqgemm_stream dispatches to it when
+// tex_stream_applies (texel range) unless BQG_STREAM_IMPL=tma.
+bool tex_stream_applies(long long m, int G, int beta);
+constexpr int kTexMinGroup = 4;
+cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
+                               float* ws, bool pdl, cudaStream_t stream);
 
 // Single-call latency form (biqgemm_latency.cu): b == 1, mu == 8, beta <= 4,
 // NB in {1,2,4,8,16}; one kernel, in-cluster push reduction.  *used = false

@@ -10,6 +10,7 @@ configs.json (the BASELINE configs' outputs/checksums on the bench_cli data,
 seeds 0x5EED / 0x5EED+1, bench_cli.cpp:106-109).
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -62,19 +63,37 @@ CONFIGS = {
     "C1": (1024, 1024, 1, 1),
     "C2": (4096, 4096, 3, 1),
     "C3": (4096, 4096, 2, 32),
-    "C4b1": (16384, 4096, 3, 1),
-    "C4b8": (16384, 4096, 3, 8),
+    # BASELINE configs[3]: the full batch sweep 1..256
+    **{f"C4b{b}": (16384, 4096, 3, b) for b in (1, 2, 4, 8, 16, 32, 64, 128, 256)},
+    # BASELINE configs[4]: the multi-GPU config (row-sharded on the GPU side)
+    "C5": (65536, 8192, 2, 8),
 }
+# Full y is stored when it is small; otherwise a strided row sample (<= ~16K
+# floats) plus the sha256 of the reference's whole y (bytes of the f32 array)
+# and its checksum.  The GPU exact path must reproduce y_sha bit-for-bit; the
+# fast path is compared with that exact y (tests/test_gpu_parity.py).
+SAMPLE_ELEMS = 16384
 
 
 def configs(ref):
+    import hashlib
+
     arrays, meta = {}, {}
+    cache = {}
     for name, (m, n, beta, b) in CONFIGS.items():
-        w = ref.random_uniform(m, n, SEED)
+        if (m, n, beta) not in cache:  # the C4 sweep shares W / keys
+            cache.clear()
+            w = ref.random_uniform(m, n, SEED)
+            cache[(m, n, beta)] = (w,) + ref.quantize_pack(w, beta, 8)
+        w, planes, alpha, keys = cache[(m, n, beta)]
         x = ref.random_normal(n, b, SEED + 1)
-        planes, alpha, keys = ref.quantize_pack(w, beta, 8)
-        y, st = ref.biqgemm(keys, alpha, n, 8, x)
+        # threads only split rows; the reference's result is bitwise
+        # independent of them (acceptance criterion 7)
+        y, st = ref.biqgemm(keys, alpha, n, 8, x, threads=os.cpu_count() or 1)
+        stride = max(1, -(-(m * b) // SAMPLE_ELEMS))
         meta[name] = dict(m=m, n=n, beta=beta, b=b, mu=8, checksum=float(np.sum(y.astype(np.float64))),
+                          y_sha=hashlib.sha256(np.ascontiguousarray(y).tobytes()).hexdigest(),
+                          y_norm=float(np.linalg.norm(y.astype(np.float64))), sample_stride=stride,
                           lookups=st["lookups"], lut_build_ops=st["lut_build_ops"],
                           keys_sha=__import__("hashlib").sha256(keys.astype(np.uint8).tobytes()).hexdigest(),
                           alpha_sha=__import__("hashlib").sha256(alpha.tobytes()).hexdigest(),
@@ -82,12 +101,15 @@ def configs(ref):
                           x_sha=__import__("hashlib").sha256(x.tobytes()).hexdigest())
         if m * b <= 200_000:
             arrays[name + "_y"] = y
-        print(name, meta[name]["checksum"])
+        else:
+            arrays[name + "_ysample"] = np.ascontiguousarray(y[::stride])
+        print(name, meta[name]["checksum"], flush=True)
     np.savez_compressed(HERE / "configs.npz", **arrays)
     (HERE / "configs.json").write_text(json.dumps(meta, indent=1))
 
 
 if __name__ == "__main__":
     r = Reference()
-    cases(r)
+    if "--configs-only" not in sys.argv:
+        cases(r)
     configs(r)
