@@ -333,22 +333,43 @@ def test_pdl_chain_and_graph(bq, port, cuda):
     assert_close(y2.cpu().numpy(), r2)
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4b1", "C4b8"])
+BASELINE_POINTS = ["C1", "C2", "C3"] + [f"C4b{b}" for b in (1, 2, 4, 8, 16, 32, 64, 128, 256)] + ["C5"]
+
+
+@pytest.mark.parametrize("name", BASELINE_POINTS)
 def test_baseline_configs(bq, cuda, name):
-    """The BASELINE configs on the bench_cli data (seeds 0x5EED/0x5EED+1):
-    exact path reproduces the reference checksum bit-for-bit; fast path within
-    the fp32 contract (golden y where stored, else the exact path's y)."""
+    """Every BASELINE config point on the bench_cli data (seeds 0x5EED /
+    0x5EED+1, bench_cli.cpp:106-109) against the REFERENCE's own output
+    (tests/golden/make_golden.py ran biqgemm::biqgemm, kernel.hpp:246-258):
+      - the GPU quantize/pack reproduces the reference's keys and alpha (sha256);
+      - the exact path reproduces the reference's y bit for bit (sha256 of the
+        whole y, and its checksum);
+      - the fast path meets the fp32 contract against that y (and the stored
+        reference rows).
+    C4 covers the whole batch sweep b = 1..256 (configs[3]); C5 is the
+    multi-GPU config (65536 x 8192, q2, b8) computed whole on one GPU."""
+    import hashlib
+
     meta = json.loads((GOLD / "configs.json").read_text())[name]
     m, n, beta, b = meta["m"], meta["n"], meta["beta"], meta["b"]
     layer = bq.PackedLinear.from_weights(bq.random_uniform(m, n, 0x5EED), beta, 8)
+    keys, alpha = layer.export()
+    assert hashlib.sha256(keys.astype(np.uint8).tobytes()).hexdigest() == meta["keys_sha"]
+    assert hashlib.sha256(alpha.tobytes()).hexdigest() == meta["alpha_sha"]
     x = bq.random_normal(n, b, 0x5EED + 1)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == meta["x_sha"]
     y_exact = layer.forward(x, exact=True)
     assert float(np.sum(y_exact.astype(np.float64))) == meta["checksum"]
+    assert hashlib.sha256(np.ascontiguousarray(y_exact).tobytes()).hexdigest() == meta["y_sha"]
     gold = np.load(GOLD / "configs.npz")
     if name + "_y" in gold.files:
         assert np.array_equal(y_exact, gold[name + "_y"])
     y = layer.forward(x)
     assert_close(y, y_exact)
+    if name + "_ysample" in gold.files:
+        ys = gold[name + "_ysample"]
+        assert np.array_equal(y_exact[:: meta["sample_stride"]], ys)
+        assert_close(y[:: meta["sample_stride"]], ys)
     layer.close()
 
 
