@@ -47,7 +47,8 @@ typedef enum bqg_status {
     BQG_ERR_TRUNCATED = 8,        /* reference: TruncatedError (model_io.hpp:26) */
     BQG_ERR_RANGE = 9,            /* reference: RangeError (model_io.hpp:30) */
     BQG_ERR_IO = 10,              /* reference: std::runtime_error (model_io.cpp:169,175) */
-    BQG_ERR_WORKSPACE = 11        /* workspace too small */
+    BQG_ERR_WORKSPACE = 11,       /* workspace too small */
+    BQG_ERR_COMM = 12             /* a collective failed or NCCL is unavailable */
 } bqg_status;
 
 /* LutLayout (lut.hpp:71) and LutBuilder (lut.hpp:73). */
@@ -171,13 +172,19 @@ int bqg_biqgemm_form(size_t m, size_t n, size_t b, unsigned beta, unsigned mu);
  * alpha, x and y -- the Q/K/V or gate/up projections of one layer, or one
  * GEMV per request of a serving batch.  Equivalent to calling
  * bqg_biqgemm_f32 once per entry; the difference is only on the device:
- * for b == 1, mu == 8, beta <= 4 the calls run in ONE persistent kernel
- * whose key stream runs ahead across call boundaries (no per-call kernel
- * handoff), followed by one fixed-order epilogue kernel.  Other shapes run
- * the single-call kernels back to back.  h_calls is a HOST array (copied
- * into the launch; graph-capturable); entries' device pointers must stay
- * valid until the stream reaches the work.  y is bitwise identical to the
- * single-call stream form and deterministic. */
+ * for b == 1, mu == 8, beta <= 4 and count >= 4 the calls run in ONE
+ * persistent kernel per 512 calls (keys through the texture pipe, the last
+ * CTA to finish a call sums its partials: biqgemm_tex.cu); fewer calls run
+ * the TMA-ring kernel plus its epilogue kernel.  Other shapes run the
+ * single-call kernels back to back.  h_calls is a HOST array (copied into
+ * the launch; graph-capturable); entries' device pointers must stay valid
+ * until the stream reaches the work; d_keys_tiled 16-byte aligned.  y is
+ * bitwise identical to the single-call stream form and deterministic.
+ * Workspace: bqg_biqgemm_grouped_workspace_bytes(); its first 2 KiB hold
+ * per-call completion counters that must be ZERO before the workspace's
+ * first use (cudaMemset at allocation; the kernels leave them zero).  A
+ * workspace address the library has not seen before is zeroed on `stream`
+ * as a safety net. */
 typedef struct bqg_call {
     const uint8_t* d_keys_tiled;
     const float* d_alpha; /* NULL = plane mode (alpha = 1) */
@@ -269,6 +276,53 @@ int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, const float*
 /* Device-resident forward on a caller stream (no copies, no sync). */
 int bqg_layer_forward_device(bqg_layer* layer, const float* d_x, size_t x_rows, size_t b, float* d_y,
                              int exact, int pdl, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * Output rows (m) sharded across ranks, one process per GPU (north_star;
+ * the reference's row-partitioned workers, kernel.hpp:80-82,162-176).
+ * Rank r owns rows [r*R, min(m, (r+1)*R)), R = 32*ceil(ceil(m/32)/nranks):
+ * 32-row aligned, so y is bitwise identical for any nranks. */
+int bqg_shard_rows(size_t m, int nranks, int rank, size_t* row_begin, size_t* row_end,
+                   size_t* rows_per_rank);
+
+/* Collectives used by the sharded call, stream-ordered on `stream`:
+ * broadcast `bytes` of d_buf from `root` in place; all-gather
+ * `bytes_per_rank` from d_send into d_recv (rank r's bytes at offset
+ * r*bytes_per_rank; d_send may alias that slot).  bqg_nccl_collectives()
+ * fills it with NCCL (ncclBroadcast / ncclAllGather over NVLink); tests can
+ * plug in their own (e.g. gloo with host staging). */
+typedef struct bqg_collectives {
+    void* ctx;
+    int (*broadcast)(void* ctx, void* d_buf, size_t bytes, int root, void* stream);
+    int (*allgather)(void* ctx, const void* d_send, void* d_recv, size_t bytes_per_rank, void* stream);
+} bqg_collectives;
+
+/* NCCL, resolved at run time (dlopen libnccl.so.2; no link-time dependency).
+ * The 128-byte unique id is created on one rank and passed to all (e.g. via
+ * torch.distributed); the communicator binds to the current CUDA device. */
+int bqg_nccl_available(void);
+int bqg_nccl_unique_id(void* h_id128);
+int bqg_nccl_comm_init(const void* h_id128, int nranks, int rank, void** comm_out);
+int bqg_nccl_comm_destroy(void* comm);
+int bqg_nccl_collectives(void* comm, bqg_collectives* out);
+
+/* One row-sharded biqgemm call (kernel.hpp:246-258 over all m rows):
+ *   1. broadcast d_x (x_rows x b) from rank 0, in place;
+ *   2. this rank's rows [row_begin, row_end) with bqg_biqgemm_f32 on its
+ *      shard (d_keys_tiled_shard / d_alpha_shard: the tiled keys and alpha of
+ *      those rows, e.g. a layer built from W[row_begin:row_end]) into block
+ *      `rank` of d_y_gather;
+ *   3. all-gather the nranks blocks of R*b floats into d_y_gather.
+ * d_y_gather holds nranks*R*b floats; its first m*b floats are y (m x b).
+ * Workspace: bqg_biqgemm_sharded_workspace_bytes().  Every rank calls it
+ * with the same (m, n, b, beta, mu). */
+size_t bqg_biqgemm_sharded_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                           int nranks);
+int bqg_biqgemm_sharded_f32(const uint8_t* d_keys_tiled_shard, const float* d_alpha_shard, float* d_x,
+                            size_t x_rows, float* d_y_gather, size_t m, size_t n, size_t b,
+                            unsigned beta, unsigned mu, int rank, int nranks,
+                            const bqg_collectives* coll, void* d_workspace, size_t workspace_bytes,
+                            void* stream);
 
 #ifdef __cplusplus
 }

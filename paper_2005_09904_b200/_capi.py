@@ -26,6 +26,7 @@ BQG_ERR_TRUNCATED = 8
 BQG_ERR_RANGE = 9
 BQG_ERR_IO = 10
 BQG_ERR_WORKSPACE = 11
+BQG_ERR_COMM = 12
 
 LUT_TABLE_MAJOR = 0
 LUT_KEY_MAJOR = 1
@@ -54,6 +55,16 @@ class KernelStats(C.Structure):
         ("query_seconds", f64),
         ("replace_seconds", f64),
     ]
+
+
+BcastFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+AllGatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class Collectives(C.Structure):
+    """bqg_collectives: the broadcast / all-gather the sharded call uses."""
+
+    _fields_ = [("ctx", C.c_void_p), ("broadcast", BcastFn), ("allgather", AllGatherFn)]
 
 
 class Call(C.Structure):
@@ -107,6 +118,15 @@ SIGNATURES = {
     "bqg_layer_device_alpha": (vp, [vp]),
     "bqg_layer_forward_host": (i32, [vp, vp, sz, sz, vp, i32, P(KernelStats)]),
     "bqg_layer_forward_device": (i32, [vp, vp, sz, sz, vp, i32, i32, vp]),
+    "bqg_shard_rows": (i32, [sz, i32, i32, P(sz), P(sz), P(sz)]),
+    "bqg_nccl_available": (i32, []),
+    "bqg_nccl_unique_id": (i32, [vp]),
+    "bqg_nccl_comm_init": (i32, [vp, i32, i32, P(vp)]),
+    "bqg_nccl_comm_destroy": (i32, [vp]),
+    "bqg_nccl_collectives": (i32, [vp, P(Collectives)]),
+    "bqg_biqgemm_sharded_workspace_bytes": (sz, [sz, sz, sz, u32, u32, i32]),
+    "bqg_biqgemm_sharded_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, i32, i32, P(Collectives), vp, sz,
+                                      vp]),
 }
 
 

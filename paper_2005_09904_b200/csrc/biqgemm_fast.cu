@@ -468,14 +468,23 @@ int plan_cpb(long long m, long long groups, int beta, long long b, int num_sms) 
     return make_plan(m, groups, beta, b, 8, num_sms).cpb;
 }
 
+// Shapes for the single-kernel cluster form.  b == 1 shapes the stream form
+// takes are excluded: the latency and stream forms combine alpha per block
+// before the block sum, the cluster form after it, and the choice must not
+// depend on m (MT) -- else a layer and its row shards could take different
+// forms and y would differ in the last bits across shardings.
+bool cluster_shape(const QueryParams& p, int mu) {
+    if (p.b == 1 && stream_supported(mu, p.beta, p.b)) return false;
+    return p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
+}
+
 int fast_form(const QueryParams& p, int mu) {
     static const int debug_flags = [] {
         const char* e = getenv("BQG_DEBUG_FLAGS");
         return e ? atoi(e) : 0;
     }();
     if (!(debug_flags & (128 | 8192 | 16384)) && latency_supported(mu, p.beta, p.b, p.NB) && latency_applies(p)) return 1;
-    const bool cluster_shape = p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
-    if (!(debug_flags & 128) && (cluster_shape || (debug_flags & 8192))) return 2;  // (if the device can co-schedule it)
+    if (!(debug_flags & 128) && (cluster_shape(p, mu) || (debug_flags & 8192))) return 2;  // (if the device can co-schedule it)
     if (!(debug_flags & (128 | 8192 | 65536)) && stream_supported(mu, p.beta, p.b)) return 4;
     return 3;
 }
@@ -502,8 +511,7 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
         cudaError_t e = launch_biqgemm_latency(p, pdl, stream, &used);
         if (e != cudaSuccess || used) return e;
     }
-    const bool cluster_shape = p.b <= 4 && p.NB >= 8 && p.NB <= 16 && p.MT <= 256;
-    if (!(debug_flags & 128) && (cluster_shape || (debug_flags & 8192))) {  // 128/8192: force a form (profiling)
+    if (!(debug_flags & 128) && (cluster_shape(p, mu) || (debug_flags & 8192))) {  // 128/8192: force a form (profiling)
         bool used = false;
         cudaError_t e = launch_biqgemm_cluster(p, mu, pdl, stream, &used);
         if (e != cudaSuccess || used) return e;

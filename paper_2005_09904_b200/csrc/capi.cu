@@ -117,6 +117,7 @@ extern "C" const char* bqg_status_string(int status) {
         case BQG_ERR_RANGE: return "value out of range";
         case BQG_ERR_IO: return "I/O error";
         case BQG_ERR_WORKSPACE: return "workspace too small";
+        case BQG_ERR_COMM: return "collective communication error";
         default: return "unknown status";
     }
 }
@@ -1175,4 +1176,166 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
         stats->replace_seconds += (t03 - t12 > 0 ? t03 - t12 : 0) * 1e-3;
     }
     return BQG_OK;
+}
+
+// ============================================================ multi-GPU
+// Row sharding (north_star): rank r owns output rows
+// [r*R, min(m, (r+1)*R)), R = 32*ceil(ceil(m/32)/nranks).  Row tiles never
+// straddle ranks, so every output's reduction tree -- and y -- is bitwise
+// identical for any number of ranks, and with EQUAL blocks the all-gathered
+// buffer's first m*b floats are y (m x b row-major) with no compaction.
+// The reference partitions rows the same way across its worker threads
+// (kernel.hpp:80-82,162-176).
+//
+// NCCL is resolved at run time (dlopen of libnccl.so.2): the library has no
+// link-time NCCL dependency, and inside a PyTorch process it shares the NCCL
+// torch already loaded.
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::once_flag g_nccl_once;
+
+const NcclApi& nccl() {
+    std::call_once(g_nccl_once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            g_nccl.why = dlerror() ? dlerror() : "libnccl.so.2 not found";
+            return;
+        }
+        auto sym = [&](const char* name) { return dlsym(h, name); };
+        g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(sym("ncclGetUniqueId"));
+        g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(sym("ncclCommInitRank"));
+        g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(sym("ncclCommDestroy"));
+        g_nccl.CommGetAsyncError = reinterpret_cast<decltype(g_nccl.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+        g_nccl.Broadcast = reinterpret_cast<decltype(g_nccl.Broadcast)>(sym("ncclBroadcast"));
+        g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(sym("ncclAllGather"));
+        g_nccl.GetErrorString = reinterpret_cast<decltype(g_nccl.GetErrorString)>(sym("ncclGetErrorString"));
+        g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Broadcast &&
+                    g_nccl.AllGather && g_nccl.GetErrorString && g_nccl.CommGetAsyncError;
+        if (!g_nccl.ok) g_nccl.why = "libnccl.so.2 lacks an expected symbol";
+    });
+    return g_nccl;
+}
+
+int nccl_err(ncclResult_t r, const char* what) {
+    return set_err(BQG_ERR_COMM, "%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "NCCL error");
+}
+
+int nccl_bcast(void* ctx, void* d_buf, size_t bytes, int root, void* stream) {
+    const ncclResult_t r = nccl().Broadcast(d_buf, d_buf, bytes, ncclUint8, root, static_cast<ncclComm_t>(ctx),
+                                            as_stream(stream));
+    return r == ncclSuccess ? BQG_OK : nccl_err(r, "ncclBroadcast");
+}
+
+int nccl_allgather(void* ctx, const void* d_send, void* d_recv, size_t bytes_per_rank, void* stream) {
+    const ncclResult_t r = nccl().AllGather(d_send, d_recv, bytes_per_rank, ncclUint8, static_cast<ncclComm_t>(ctx),
+                                            as_stream(stream));
+    return r == ncclSuccess ? BQG_OK : nccl_err(r, "ncclAllGather");
+}
+
+}  // namespace
+
+extern "C" int bqg_nccl_available(void) { return nccl().ok ? 1 : 0; }
+
+extern "C" int bqg_nccl_unique_id(void* h_id) {
+    if (!h_id) return set_err(BQG_ERR_INVALID_ARGUMENT, "nccl_unique_id: null pointer");
+    if (!nccl().ok) return set_err(BQG_ERR_COMM, "NCCL unavailable: %s", nccl().why.c_str());
+    ncclUniqueId id;
+    const ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_err(r, "ncclGetUniqueId");
+    std::memcpy(h_id, &id, sizeof(id));
+    return BQG_OK;
+}
+
+extern "C" int bqg_nccl_comm_init(const void* h_id, int nranks, int rank, void** comm_out) {
+    if (!h_id || !comm_out) return set_err(BQG_ERR_INVALID_ARGUMENT, "nccl_comm_init: null pointer");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "nccl_comm_init: rank %d of %d", rank, nranks);
+    if (!nccl().ok) return set_err(BQG_ERR_COMM, "NCCL unavailable: %s", nccl().why.c_str());
+    BQG_NEED_DEVICE();
+    ncclUniqueId id;
+    std::memcpy(&id, h_id, sizeof(id));
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = nccl().CommInitRank(&c, nranks, id, rank);  // on the current device
+    if (r != ncclSuccess) return nccl_err(r, "ncclCommInitRank");
+    *comm_out = c;
+    return BQG_OK;
+}
+
+extern "C" int bqg_nccl_comm_destroy(void* comm) {
+    if (!comm) return BQG_OK;
+    if (!nccl().ok) return set_err(BQG_ERR_COMM, "NCCL unavailable: %s", nccl().why.c_str());
+    const ncclResult_t r = nccl().CommDestroy(static_cast<ncclComm_t>(comm));
+    return r == ncclSuccess ? BQG_OK : nccl_err(r, "ncclCommDestroy");
+}
+
+extern "C" int bqg_nccl_collectives(void* comm, bqg_collectives* out) {
+    if (!comm || !out) return set_err(BQG_ERR_INVALID_ARGUMENT, "nccl_collectives: null pointer");
+    if (!nccl().ok) return set_err(BQG_ERR_COMM, "NCCL unavailable: %s", nccl().why.c_str());
+    out->ctx = comm;
+    out->broadcast = nccl_bcast;
+    out->allgather = nccl_allgather;
+    return BQG_OK;
+}
+
+extern "C" int bqg_shard_rows(size_t m, int nranks, int rank, size_t* row_begin, size_t* row_end,
+                              size_t* rows_per_rank) {
+    if (m == 0 || nranks < 1 || rank < 0 || rank >= nranks)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "shard_rows: m %zu, rank %d of %d", m, rank, nranks);
+    const size_t tiles = (m + 31) / 32;
+    const size_t R = 32 * ((tiles + static_cast<size_t>(nranks) - 1) / static_cast<size_t>(nranks));
+    if (row_begin) *row_begin = std::min(m, static_cast<size_t>(rank) * R);
+    if (row_end) *row_end = std::min(m, static_cast<size_t>(rank + 1) * R);
+    if (rows_per_rank) *rows_per_rank = R;
+    return BQG_OK;
+}
+
+extern "C" size_t bqg_biqgemm_sharded_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                                      int nranks) {
+    size_t R = 0;
+    if (bqg_shard_rows(m, nranks, 0, nullptr, nullptr, &R) != BQG_OK) return 0;
+    return bqg_biqgemm_workspace_bytes(std::min(R, m), n, b, beta, mu);
+}
+
+extern "C" int bqg_biqgemm_sharded_f32(const uint8_t* d_keys_tiled_shard, const float* d_alpha_shard, float* d_x,
+                                       size_t x_rows, float* d_y_gather, size_t m, size_t n, size_t b,
+                                       unsigned beta, unsigned mu, int rank, int nranks,
+                                       const bqg_collectives* coll, void* d_ws, size_t ws_bytes, void* stream) {
+    size_t lo = 0, hi = 0, R = 0;
+    int s = bqg_shard_rows(m, nranks, rank, &lo, &hi, &R);
+    if (s) return s;
+    if (!coll || !coll->broadcast || !coll->allgather)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: collectives missing");
+    if (!d_x || !d_y_gather) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null pointer");
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    // 1. x from rank 0 to every rank (in place; a 1-rank group runs it too,
+    //    so the collective path is exercised on a single GPU)
+    s = coll->broadcast(coll->ctx, d_x, x_rows * b * sizeof(float), 0, stream);
+    if (s) return s;
+    // 2. this rank's rows into its block of the gather buffer
+    float* y_mine = d_y_gather + static_cast<size_t>(rank) * R * b;
+    if (hi > lo) {
+        s = bqg_biqgemm_f32(d_keys_tiled_shard, d_alpha_shard, d_x, x_rows, y_mine, hi - lo, n, b, beta, mu, d_ws,
+                            ws_bytes, 0, stream);
+        if (s) return s;
+    }
+    // 3. the row blocks to every rank: the buffer's first m*b floats are y
+    return coll->allgather(coll->ctx, y_mine, d_y_gather, R * b * sizeof(float), stream);
 }

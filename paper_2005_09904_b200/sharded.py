@@ -1,22 +1,29 @@
 """Multi-GPU BiQGEMM: weight rows sharded across ranks.
 
-One process per GPU (torch.distributed; NCCL over NVLink on the B200 box).
-The output dimension m is split into contiguous, 32-row-aligned blocks
-(row tiles never straddle ranks, so every output's reduction tree -- and
-therefore y -- is bitwise identical for any number of ranks).  Each rank
-holds only its rows' packed keys and alphas, receives x by broadcast from
-rank 0, runs the fused kernel on its rows, and the row blocks are assembled
-with an all-gather.  Rows are independent (per-row alpha, paper Eq. 2), so no
-reduction is ever needed; that is also why the reference partitions rows
-across its worker threads (kernel.hpp:80-82,165-173).
+One process per GPU.  The output dimension m is split into equal,
+32-row-aligned blocks of R = 32*ceil(ceil(m/32)/world) rows (the last rank
+takes the remainder; row tiles never straddle ranks, so every output's
+reduction tree -- and therefore y -- is bitwise identical for any number of
+ranks).  Each rank holds only its rows' packed keys and alphas, receives x by
+broadcast from rank 0, runs the fused kernel on its rows, and the row blocks
+are all-gathered: with equal blocks the gathered buffer's first m*b floats
+ARE y.  Rows are independent (per-row alpha, paper Eq. 2), so no reduction is
+ever needed; that is also why the reference partitions rows across its
+worker threads (kernel.hpp:80-82,162-176).
 
-The per-rank compute is pluggable only so the CPU (gloo) tests can exercise
-the sharding/collective logic without a GPU; production code always passes
-the CUDA path (``device_compute``), which fails loudly if the library is not
-built.
+Two drivers of the same decomposition:
+  * ``ShardedLinear`` -- the product path: ``bqg_biqgemm_sharded_f32``
+    through the C ABI (broadcast -> kernel -> all-gather, stream-ordered),
+    with NCCL collectives (``NcclComm``; ncclBroadcast / ncclAllGather over
+    NVLink) or any ``bqg_collectives`` provider (``TorchCollectives``: the
+    same calls through torch.distributed, e.g. gloo for single-GPU tests).
+  * ``ShardedBiQGEMM`` -- the same plan with a pluggable per-rank compute, so
+    the CPU (gloo) tests can run the sharding/collective logic with the
+    oracle and no GPU.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 from typing import Callable
 
@@ -27,15 +34,17 @@ ROW_ALIGN = 32
 
 
 def shard_bounds(m: int, world: int, align: int = ROW_ALIGN) -> list[int]:
-    """Contiguous row blocks, boundaries on multiples of `align` (the last
-    block absorbs the ragged tail).  len = world + 1, bounds[0] = 0,
-    bounds[-1] = m; a rank may own zero rows when m is small."""
+    """Row blocks of R = align*ceil(ceil(m/align)/world) rows: rank r owns
+    [min(m, r*R), min(m, (r+1)*R)).  len = world + 1, bounds[0] = 0,
+    bounds[-1] = m; a rank may own zero rows when m is small.  Same law as
+    bqg_shard_rows in the C ABI."""
+    R = rows_per_rank(m, world, align)
+    return [min(m, r * R) for r in range(world)] + [m]
+
+
+def rows_per_rank(m: int, world: int, align: int = ROW_ALIGN) -> int:
     tiles = (m + align - 1) // align
-    out = []
-    for r in range(world + 1):
-        out.append(min(m, (tiles * r // world) * align))
-    out[-1] = m
-    return out
+    return align * ((tiles + world - 1) // world)
 
 
 @dataclass
@@ -53,11 +62,13 @@ class ShardPlan:
 
     @property
     def max_rows(self) -> int:
-        return max(self.bounds[r + 1] - self.bounds[r] for r in range(self.world))
+        """Rows per gather block (R): every rank contributes R*b floats."""
+        return rows_per_rank(self.m, self.world)
 
 
 class ShardedBiQGEMM:
-    """Row-sharded y = sum_i alpha_i o (B_i . x) across a process group.
+    """Row-sharded y = sum_i alpha_i o (B_i . x) across a process group, with
+    a pluggable per-rank compute (the CPU tests pass the oracle).
 
     compute(x_dev, y_local) must fill y_local [rows, b] for this rank's rows.
     """
@@ -86,8 +97,7 @@ class ShardedBiQGEMM:
             return y_pad[: self.plan.m].clone()
         gathered = torch.empty((world * R, b), dtype=torch.float32, device=self.device)
         dist.all_gather_into_tensor(gathered, y_pad, group=self.group)
-        parts = [gathered[r * R: r * R + (self.plan.bounds[r + 1] - self.plan.bounds[r])] for r in range(world)]
-        return torch.cat(parts, dim=0)
+        return gathered[: self.plan.m].clone()
 
 
 def device_compute(layer, pdl: bool = False):
@@ -98,3 +108,171 @@ def device_compute(layer, pdl: bool = False):
         layer.forward_device(x_dev, y_local, pdl=pdl)
 
     return run
+
+
+# ------------------------------------------------------------ C-ABI path
+
+
+class NcclComm:
+    """An NCCL communicator created through the library (bqg_nccl_*): the
+    128-byte unique id is made on rank 0 and sent to every rank over the
+    existing torch.distributed group; the communicator binds to the current
+    CUDA device."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        from . import _capi
+
+        self._capi = _capi
+        lib = _capi.lib
+        if not lib.bqg_nccl_available():
+            raise RuntimeError("NCCL (libnccl.so.2) is not available")
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _capi.check(lib.bqg_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        comm = C.c_void_p()
+        _capi.check(lib.bqg_nccl_comm_init(uid, world, rank, C.byref(comm)))
+        self.comm = comm
+        self.coll = _capi.Collectives()
+        _capi.check(lib.bqg_nccl_collectives(comm, C.byref(self.coll)))
+
+    def collectives(self):
+        return self.coll
+
+    def close(self):
+        if self.comm:
+            self._capi.check(self._capi.lib.bqg_nccl_comm_destroy(self.comm))
+            self.comm = None
+
+
+class TorchCollectives:
+    """bqg_collectives backed by torch.distributed (any backend).  The C call
+    passes raw device pointers; they are resolved against the registered
+    tensors.  With gloo the data is staged through host memory -- a test
+    path (single-GPU multi-rank), not a fast one."""
+
+    def __init__(self, group=None, host_staging: bool | None = None):
+        from . import _capi
+
+        self.group = group
+        be = dist.get_backend(group) if dist.is_initialized() else "gloo"
+        self.host = (be == "gloo") if host_staging is None else host_staging
+        self._bufs: dict[int, torch.Tensor] = {}
+        self._bc = _capi.BcastFn(self._broadcast)
+        self._ag = _capi.AllGatherFn(self._allgather)
+        self.coll = _capi.Collectives(None, self._bc, self._ag)
+
+    def register(self, *tensors: torch.Tensor):
+        for t in tensors:
+            if t is not None:
+                self._bufs[t.data_ptr()] = t
+
+    def collectives(self):
+        return self.coll
+
+    def _view(self, ptr: int, nbytes: int) -> torch.Tensor:
+        for t in self._bufs.values():
+            base = t.data_ptr()
+            if base <= ptr and ptr + nbytes <= base + t.numel() * t.element_size():
+                flat = t.view(-1).view(torch.uint8)
+                return flat[ptr - base: ptr - base + nbytes]
+        raise KeyError(f"pointer {ptr:#x} not in a registered tensor")
+
+    def _broadcast(self, ctx, buf, nbytes, root, stream):
+        try:
+            torch.cuda.synchronize()
+            v = self._view(buf, nbytes)
+            t = v.cpu() if self.host else v
+            dist.broadcast(t, src=root, group=self.group)
+            if self.host:
+                v.copy_(t)
+                torch.cuda.synchronize()
+            return 0
+        except Exception:  # pragma: no cover - surfaced as BQG_ERR_COMM
+            return 12
+
+    def _allgather(self, ctx, send, recv, nbytes, stream):
+        try:
+            torch.cuda.synchronize()
+            world = dist.get_world_size(self.group)
+            s = self._view(send, nbytes)
+            r = self._view(recv, nbytes * world)
+            if self.host:
+                rc = torch.empty(nbytes * world, dtype=torch.uint8)
+                dist.all_gather_into_tensor(rc, s.cpu().clone(), group=self.group)
+                r.copy_(rc)
+                torch.cuda.synchronize()
+            else:
+                dist.all_gather_into_tensor(r, s.clone(), group=self.group)
+            return 0
+        except Exception:  # pragma: no cover
+            return 12
+
+
+class ShardedLinear:
+    """This rank's row shard of an m x n layer plus the sharded C-ABI call
+    (bqg_biqgemm_sharded_f32): x broadcast from rank 0, the fused kernel on
+    the shard, y all-gathered -- stream-ordered, one call."""
+
+    def __init__(self, shard_layer, m: int, n: int, beta: int, mu: int, rank: int, world: int, collectives,
+                 device=None):
+        from . import biqgemm as bq
+
+        self.bq = bq
+        self.layer = shard_layer  # PackedLinear of rows [lo, hi) (None when the rank owns no rows)
+        self.m, self.n, self.beta, self.mu = m, n, beta, mu
+        self.rank, self.world = rank, world
+        self.plan = ShardPlan.make(m, world)
+        self.coll_provider = collectives
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._ws = {}
+
+    @classmethod
+    def from_weights(cls, w_full, beta, mu, rank, world, collectives):
+        """Quantize/pack only this rank's rows of W (the per-row algorithm,
+        quantize.hpp:27-58, needs nothing from other rows)."""
+        import numpy as np
+
+        from . import biqgemm as bq
+
+        m, n = w_full.shape
+        lo, hi = ShardPlan.make(m, world).rows(rank)
+        layer = bq.PackedLinear.from_weights(np.ascontiguousarray(w_full[lo:hi]), beta, mu) if hi > lo else None
+        return cls(layer, m, n, beta, mu, rank, world, collectives)
+
+    def gather_buffer(self, b: int) -> torch.Tensor:
+        """[world*R, b]: y is its first m rows after forward()."""
+        return torch.empty((self.world * self.plan.max_rows, b), dtype=torch.float32, device=self.device)
+
+    def workspace(self, b: int):
+        if b not in self._ws:
+            bq = self.bq
+            self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_workspace_bytes(
+                self.m, self.n, b, self.beta, self.mu, self.world)), device=self.device)
+        return self._ws[b]
+
+    def forward_device(self, x: torch.Tensor, y_gather: torch.Tensor, stream=None) -> torch.Tensor:
+        """x: [n, b] device buffer (rank 0's contents are broadcast into it);
+        returns the view y_gather[:m]."""
+        bq = self.bq
+        x_rows, b = x.shape
+        assert x.dtype == torch.float32 and x.is_contiguous() and x.device == self.device
+        assert y_gather.shape == (self.world * self.plan.max_rows, b) and y_gather.is_contiguous()
+        if isinstance(self.coll_provider, TorchCollectives):
+            self.coll_provider.register(x, y_gather)
+        ws = self.workspace(b)
+        keys = self.layer.device_tiled_keys if self.layer is not None else None
+        alpha = self.layer.device_alpha if self.layer is not None else None
+        coll = self.coll_provider.collectives()
+        bq.check(bq.lib.bqg_biqgemm_sharded_f32(keys, alpha, x.data_ptr(), x_rows, y_gather.data_ptr(), self.m,
+                                                self.n, b, self.beta, self.mu, self.rank, self.world,
+                                                C.byref(coll), ws.ptr(), ws.nbytes, bq._stream(stream)))
+        return y_gather[: self.m]
+
+    def close(self):
+        if self.layer is not None:
+            self.layer.close()
+            self.layer = None

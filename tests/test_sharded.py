@@ -14,17 +14,41 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2005_09904_b200.sharded import ShardPlan, ShardedBiQGEMM, shard_bounds
+from paper_2005_09904_b200.sharded import ShardPlan, ShardedBiQGEMM, rows_per_rank, shard_bounds
 
 
 def test_shard_bounds():
     for m in (1, 31, 32, 33, 100, 4096, 65536, 1000):
         for world in (1, 2, 3, 4, 8):
             b = shard_bounds(m, world)
+            R = rows_per_rank(m, world)
             assert b[0] == 0 and b[-1] == m and len(b) == world + 1
             assert all(b[i] <= b[i + 1] for i in range(world))
-            assert all(v % 32 == 0 for v in b[:-1])
+            assert all(v % 32 == 0 or v == m for v in b[:-1])  # empty trailing ranks start at m
+            # equal blocks of R rows (the last takes the rest): the gathered
+            # [world*R, b] buffer's first m rows are y
+            assert all(b[i + 1] - b[i] == R for i in range(world) if b[i + 1] < m)
+            assert R % 32 == 0 and world * R >= m
     assert shard_bounds(65536, 8) == [8192 * i for i in range(9)]
+
+
+def test_shard_rows_c_abi_matches():
+    """bqg_shard_rows (the C ABI's plan, host-only) == the Python plan."""
+    import ctypes as C
+
+    from paper_2005_09904_b200 import _capi
+
+    for m in (1, 33, 100, 4097, 65536, 1000):
+        for world in (1, 2, 3, 8):
+            bnd = shard_bounds(m, world)
+            for r in range(world):
+                lo, hi, R = C.c_size_t(), C.c_size_t(), C.c_size_t()
+                _capi.check(_capi.lib.bqg_shard_rows(m, world, r, C.byref(lo), C.byref(hi), C.byref(R)))
+                assert (lo.value, hi.value, R.value) == (bnd[r], bnd[r + 1], rows_per_rank(m, world))
+    with pytest.raises(_capi.InvalidArgument):
+        _capi.check(_capi.lib.bqg_shard_rows(0, 2, 0, None, None, None))
+    with pytest.raises(_capi.InvalidArgument):
+        _capi.check(_capi.lib.bqg_shard_rows(10, 2, 2, None, None, None))
 
 
 def _free_port():
@@ -88,11 +112,15 @@ def test_gloo_sharded_matches_single(world, m, port):
 
 
 @pytest.mark.gpu
-def test_device_shards_concatenate_bitwise(bq, cuda):
-    """Production compute on every shard of an 8-way plan == the unsharded y."""
+@pytest.mark.parametrize("m,n,beta,b", [(2000, 1500, 3, 1), (16384, 3072, 3, 1), (4096, 4096, 2, 2), (3000, 2100, 2, 8)])
+def test_device_shards_concatenate_bitwise(bq, cuda, m, n, beta, b):
+    """Production compute on every shard of a 2/4/8-way plan == the unsharded
+    y, bit for bit -- including shapes whose shards and whole layer would
+    fall on different sides of a kernel-form boundary (16384 x 3072: NB = 12,
+    MT 512 whole vs 256 per half)."""
     from paper_2005_09904_b200.sharded import device_compute
 
-    m, n, beta, mu, b = 2000, 1500, 3, 8, 1
+    mu = 8
     w = bq.random_uniform(m, n, 3)
     x = torch.from_numpy(bq.random_normal(n, b, 4)).cuda()
     full = bq.PackedLinear.from_weights(w, beta, mu)
@@ -111,3 +139,82 @@ def test_device_shards_concatenate_bitwise(bq, cuda):
             parts.append(y)
             shard.close()
         assert torch.equal(torch.cat(parts), y_full)
+
+
+def _native_worker(rank, world, port, m, n, beta, b, out_q):
+    """One rank of a single-GPU multi-process run of the C-ABI sharded call
+    with gloo collectives (host staging): the production data path except
+    that NCCL is replaced by torch.distributed."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _native_worker_body(rank, world, m, n, beta, b, out_q)
+    except Exception as e:  # report instead of leaving the parent waiting
+        out_q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _native_worker_body(rank, world, m, n, beta, b, out_q):
+    if True:
+        import paper_2005_09904_b200.biqgemm as bq
+        from paper_2005_09904_b200.sharded import ShardedLinear, TorchCollectives
+
+        w = bq.random_uniform(m, n, 77)
+        coll = TorchCollectives()
+        sh = ShardedLinear.from_weights(w, beta, 8, rank, world, coll)
+        x_h = bq.random_normal(n, b, 78)
+        x = torch.from_numpy(x_h).cuda() if rank == 0 else torch.zeros((n, b), device="cuda")
+        yg = sh.gather_buffer(b)
+        y = sh.forward_device(x, yg).cpu().numpy()
+        torch.cuda.synchronize()
+        full = bq.PackedLinear.from_weights(w, beta, 8)
+        y_full = full.forward(x_h)
+        out_q.put((rank, bool(np.array_equal(y, y_full)), float(np.abs(y - y_full).max())))
+        full.close()
+        sh.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,m,n,beta,b", [(2, 4096, 4096, 3, 1), (3, 1000, 777, 2, 1), (2, 3000, 1024, 2, 4)])
+def test_native_sharded_single_gpu_gloo(cuda, world, m, n, beta, b):
+    """bqg_biqgemm_sharded_f32 with `world` ranks on one GPU (gloo collectives
+    through the bqg_collectives vtable): every rank's y == the unsharded y,
+    bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_native_worker, args=(r, world, portn, m, n, beta, b, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, diff in res:
+        assert ok, f"rank {rank}: max |dy| {diff}"
+
+
+@pytest.mark.gpu
+def test_native_sharded_nccl_one_rank(bq, cuda):
+    """The NCCL collectives (dlopen'ed libnccl.so.2) on a 1-rank communicator:
+    ncclBroadcast and ncclAllGather run inside bqg_biqgemm_sharded_f32; y ==
+    the layer's own y bitwise."""
+    from paper_2005_09904_b200.sharded import NcclComm, ShardedLinear
+
+    assert bq.lib.bqg_nccl_available() == 1
+    m, n, beta, b = 4096, 4096, 3, 1
+    w = bq.random_uniform(m, n, 5)
+    comm = NcclComm(0, 1)
+    sh = ShardedLinear.from_weights(w, beta, 8, 0, 1, comm)
+    x_h = bq.random_normal(n, b, 6)
+    x = torch.from_numpy(x_h).cuda()
+    yg = sh.gather_buffer(b)
+    y = sh.forward_device(x, yg).cpu().numpy()
+    full = bq.PackedLinear.from_weights(w, beta, 8)
+    assert np.array_equal(y, full.forward(x_h))
+    full.close()
+    sh.close()
+    comm.close()
