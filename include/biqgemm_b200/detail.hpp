@@ -6,6 +6,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -88,6 +90,46 @@ public:
 private:
     void* ptr_ = nullptr;
     std::size_t bytes_ = 0;
+};
+
+// The device copy of a host model (PackedLinear / KeyMatrix), created on the
+// first multiply and reused.  A COPY of the owning object starts empty (the
+// copy's keys may be changed independently of the original's), creation is
+// serialised (two threads multiplying with one const model build one device
+// copy), and the copy is tagged with the host buffer it was made from: a
+// model whose key storage was reallocated or resized gets a fresh one.
+// In-place edits of keys/alphas need reset_device() on the owner.
+class DeviceCache {
+public:
+    DeviceCache() = default;
+    DeviceCache(const DeviceCache&) {}
+    DeviceCache& operator=(const DeviceCache&) {
+        reset();
+        return *this;
+    }
+    bool operator==(const DeviceCache&) const { return true; }  // not part of the model's value
+    template <class Make>
+    std::shared_ptr<void> get(const void* tag, std::size_t tag_size, Make&& make) const {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!p_ || tag != tag_ || tag_size != tag_size_) {
+            p_ = make();
+            tag_ = tag;
+            tag_size_ = tag_size;
+        }
+        return p_;
+    }
+    void reset() const {
+        std::lock_guard<std::mutex> lk(mu_);
+        p_.reset();
+        tag_ = nullptr;
+        tag_size_ = 0;
+    }
+
+private:
+    mutable std::mutex mu_;
+    mutable std::shared_ptr<void> p_;
+    mutable const void* tag_ = nullptr;
+    mutable std::size_t tag_size_ = 0;
 };
 
 }  // namespace detail

@@ -9,8 +9,10 @@
 //     epilogue, fp32 tables; ||y - y_ref||_F / ||y_ref||_F <= 1e-5);
 //   - T = double, mu > 8, or KernelOptions::exact : the exact path (fp64
 //     tables and accumulation in the reference's order: bit-identical y).
-// A PackedLinear uploads itself to the device on first use and keeps the
-// device copy; call reset_device() after mutating keys/alphas in place.
+// A PackedLinear (and a KeyMatrix used with biqgemm_plane) uploads itself to
+// the device on first use and keeps the device copy; call reset_device()
+// after mutating keys/alphas in place.  KernelOptions::builder = Naive runs
+// the exact path with the reference's naive tables.
 // KernelOptions::threads is accepted and ignored (the GPU decides its own
 // parallelism); deterministic is always true; budget_bytes is validated as in
 // the reference; TileShape is validated but does not change the result (the
@@ -53,9 +55,12 @@ struct OpCounters {
     }
 };
 
-// Phase split on the GPU: query_seconds = the fused kernel(s) (LUT build and
-// query are one kernel; build_seconds stays 0), replace_seconds = x upload +
-// y download.
+// Phase split on the GPU (kernel.hpp:41-46).  Exact path (double, mu > 8,
+// KernelOptions::exact, or builder = Naive): build = the LUT kernels, query =
+// the lookup kernels, replace = setup + alpha epilogue + x upload + y
+// download -- the reference's split.  Fast path: the LUT build runs inside the
+// query kernel (builder warps overlap the gather), so build_seconds stays 0
+// and query_seconds is the fused kernel.
 struct KernelStats {
     OpCounters ops;
     double build_seconds = 0.0;
@@ -66,6 +71,10 @@ struct KernelStats {
 struct KernelOptions {
     std::size_t threads = 1;  // ignored on the GPU
     bool deterministic = true;
+    // Dp: the fast path (fp32 DP tables) or, with `exact`, fp64 DP tables.
+    // Naive (the reference's ablation builder, lut.hpp:31-43): fp64 naive
+    // tables on the exact path -- y bit-identical to the reference run with
+    // LutBuilder::Naive, lut_build_ops = 2^mu * mu per table (kernel.hpp:158).
     LutBuilder builder = LutBuilder::Dp;
     std::size_t budget_bytes = 0;  // 0 disables the working-set check
     bool exact = false;            // extension: force the fp64 bit-exact path
@@ -86,7 +95,7 @@ struct PackedLinear {
     unsigned mu = 0;
     std::vector<KeyMatrix> keys;         // one per plane
     std::vector<std::vector<T>> alphas;  // one length-m vector per plane
-    mutable std::shared_ptr<void> device_cache;
+    detail::DeviceCache device_cache;    // device copy, made on the first multiply (copies start empty)
     void reset_device() const { device_cache.reset(); }
 };
 
@@ -134,11 +143,12 @@ inline std::vector<std::uint8_t> narrow_keys(const std::vector<const KeyMatrix*>
 }
 
 // detail::run (kernel.hpp:116-204): validation in the reference's order, then
-// the device multiply.  `cache` holds the device copy of the model.
+// the device multiply.  `cache` holds the device copy of the model, tagged
+// with the first plane's key storage.
 template <typename T>
 Matrix<T> run(const std::vector<const KeyMatrix*>& planes, const std::vector<const std::vector<T>*>& alphas,
               std::size_t n, const Matrix<T>& x, const TileShape& tile, const KernelOptions& opts, KernelStats* stats,
-              std::shared_ptr<void>& cache) {
+              const DeviceCache& cache) {
     const KeyMatrix& k0 = *planes[0];
     const std::size_t m = k0.m, groups = k0.groups, b = x.cols();
     const unsigned mu = k0.mu;
@@ -153,33 +163,28 @@ Matrix<T> run(const std::vector<const KeyMatrix*>& planes, const std::vector<con
     }
     const unsigned beta = static_cast<unsigned>(planes.size());
     if (n == 0) n = groups * mu;  // plane mode: only the padded width is known
+    const bool naive = opts.builder == LutBuilder::Naive;
+    const void* tag = k0.keys.data();
+    const std::size_t tag_size = k0.keys.size() * beta + (alphas.empty() ? 0 : alphas[0]->size());
     Matrix<T> y(m, b);
+    bqg_kernel_stats st{};
     if constexpr (std::is_same_v<T, float>) {
-        if (!cache) {
-            auto L = std::make_shared<LayerF32>();
+        auto L = cache.get(tag, tag_size, [&] {
+            auto h = std::make_shared<LayerF32>();
             const auto keys = narrow_keys(planes, mu);
             std::vector<float> a;
             if (!alphas.empty()) {
                 a.reserve(beta * m);
                 for (auto* v : alphas) a.insert(a.end(), v->begin(), v->end());
             }
-            check(bqg_layer_create_from_keys(keys.data(), alphas.empty() ? nullptr : a.data(), m, n, beta, mu, &L->h));
-            cache = L;
-        }
-        bqg_kernel_stats st{};
-        check(bqg_layer_forward_host(static_cast<LayerF32*>(cache.get())->h, x.data(), x.rows(), b, y.data(),
-                                     opts.exact ? 1 : 0, &st));
-        if (stats) {
-            stats->ops.lut_build_ops += st.lut_build_ops;
-            stats->ops.lookups += st.lookups;
-            stats->ops.accumulate_ops += st.accumulate_ops;
-            stats->ops.fma_ops += st.fma_ops;
-            stats->build_seconds += st.build_seconds;
-            stats->query_seconds += st.query_seconds;
-            stats->replace_seconds += st.replace_seconds;
-        }
+            check(bqg_layer_create_from_keys(keys.data(), alphas.empty() ? nullptr : a.data(), m, n, beta, mu, &h->h));
+            return std::static_pointer_cast<void>(h);
+        });
+        const int path = naive ? BQG_FORWARD_EXACT_NAIVE : (opts.exact ? BQG_FORWARD_EXACT : BQG_FORWARD_FAST);
+        check(bqg_layer_forward_host(static_cast<LayerF32*>(L.get())->h, x.data(), x.rows(), b, y.data(), path,
+                                     stats ? &st : nullptr));
     } else {
-        if (!cache) {
+        auto Mp = cache.get(tag, tag_size, [&] {
             auto M = std::make_shared<ModelF64>();
             const auto keys = narrow_keys(planes, mu);
             M->keys = DeviceBuffer(keys.data(), keys.size());
@@ -188,30 +193,32 @@ Matrix<T> run(const std::vector<const KeyMatrix*>& planes, const std::vector<con
                 for (auto* v : alphas) a.insert(a.end(), v->begin(), v->end());
                 M->alpha = DeviceBuffer(a.data(), a.size() * sizeof(double));
             }
-            cache = M;
-        }
-        auto* M = static_cast<ModelF64*>(cache.get());
+            return std::static_pointer_cast<void>(M);
+        });
+        auto* M = static_cast<ModelF64*>(Mp.get());
         const auto t0 = std::chrono::steady_clock::now();
         DeviceBuffer d_x(x.data(), x.rows() * b * sizeof(double));
         DeviceBuffer d_y(m * b * sizeof(double));
         const std::size_t ws = bqg_biqgemm_exact_workspace_bytes(m, n, b, beta, mu);
         DeviceBuffer d_ws(ws);
         const auto t1 = std::chrono::steady_clock::now();
-        check(bqg_biqgemm_exact_f64(M->keys.get(), M->alpha.get<double>(), d_x.get<double>(), x.rows(),
-                                    d_y.get<double>(), m, n, b, beta, mu, d_ws.get(), ws, nullptr));
+        check(bqg_biqgemm_exact_ex_f64(M->keys.get(), M->alpha.get<double>(), d_x.get<double>(), x.rows(),
+                                       d_y.get<double>(), m, n, b, beta, mu, naive ? BQG_LUT_NAIVE : BQG_LUT_DP,
+                                       d_ws.get(), ws, stats ? &st : nullptr, nullptr));
         cuda_check(cudaDeviceSynchronize(), "biqgemm");
         const auto t2 = std::chrono::steady_clock::now();
         d_y.download(y.data(), m * b * sizeof(double));
         const auto t3 = std::chrono::steady_clock::now();
-        if (stats) {
-            std::uint64_t ops[4];
-            check(bqg_op_counters(m, n, b, beta, mu, BQG_LUT_DP, ops));
-            stats->ops.lut_build_ops += ops[0];
-            stats->ops.lookups += ops[1];
-            stats->ops.accumulate_ops += ops[2];
-            stats->query_seconds += std::chrono::duration<double>(t2 - t1).count();
-            stats->replace_seconds += std::chrono::duration<double>((t1 - t0) + (t3 - t2)).count();
-        }
+        st.replace_seconds += std::chrono::duration<double>((t1 - t0) + (t3 - t2)).count();
+    }
+    if (stats) {
+        stats->ops.lut_build_ops += st.lut_build_ops;
+        stats->ops.lookups += st.lookups;
+        stats->ops.accumulate_ops += st.accumulate_ops;
+        stats->ops.fma_ops += st.fma_ops;
+        stats->build_seconds += st.build_seconds;
+        stats->query_seconds += st.query_seconds;
+        stats->replace_seconds += st.replace_seconds;
     }
     return y;
 }
@@ -219,11 +226,12 @@ Matrix<T> run(const std::vector<const KeyMatrix*>& planes, const std::vector<con
 }  // namespace detail
 
 // kernel.hpp:209-215: one key matrix, alpha = 1.
+// The key matrix keeps its device copy (KeyMatrix::device_cache), so
+// repeated calls on one plane upload its keys once.
 template <typename T>
 Matrix<T> biqgemm_plane(const KeyMatrix& keys, const Matrix<T>& x, const TileShape& tile, KernelStats* stats = nullptr,
                         const KernelOptions& opts = {}) {
-    std::shared_ptr<void> cache;
-    return detail::run<T>({&keys}, {}, 0, x, tile, opts, stats, cache);
+    return detail::run<T>({&keys}, {}, 0, x, tile, opts, stats, keys.device_cache);
 }
 
 // kernel.hpp:246-258: sum_i alpha_i o (B_i . X).

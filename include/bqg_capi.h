@@ -54,6 +54,8 @@ typedef enum bqg_status {
 /* LutLayout (lut.hpp:71) and LutBuilder (lut.hpp:73). */
 enum { BQG_LUT_TABLE_MAJOR = 0, BQG_LUT_KEY_MAJOR = 1 };
 enum { BQG_LUT_DP = 0, BQG_LUT_NAIVE = 1 };
+/* forward path selector (the `exact` argument of the layer entry points) */
+enum { BQG_FORWARD_FAST = 0, BQG_FORWARD_EXACT = 1, BQG_FORWARD_EXACT_NAIVE = 2 };
 
 const char* bqg_status_string(int status);
 const char* bqg_last_error_message(void);
@@ -142,6 +144,18 @@ int bqg_build_lut_f64x(const double* d_x, size_t x_rows, size_t b, unsigned mu, 
                        size_t count, int layout, int builder, double* d_entries, uint64_t* ops,
                        void* stream);
 
+typedef struct bqg_kernel_stats {
+    /* OpCounters (kernel.hpp:23-36), exact, computed analytically with the
+     * builder's law (Dp: 2^mu + mu - 1, Naive: 2^mu * mu per table) */
+    uint64_t lut_build_ops, lookups, accumulate_ops, fma_ops;
+    /* KernelStats phase seconds (kernel.hpp:41-46), CUDA-event timed.
+     * Exact path: build = the LUT kernels, query = the lookup kernels,
+     * replace = setup + alpha epilogue + H2D of x + D2H of y.  Fast path: the
+     * LUT build runs INSIDE the query kernel (builder warps overlap the
+     * gather), so build_seconds stays 0 and query_seconds is that kernel. */
+    double build_seconds, query_seconds, replace_seconds;
+} bqg_kernel_stats;
+
 /* The BiQGEMM multiply, biqgemm (kernel.hpp:246-258) / biqgemm_plane
  * (kernel.hpp:209-215 when d_alpha == NULL, alpha = 1):
  *     y(r, c) = sum_i alpha_i[r] * sum_g LUT_g,c[key_i(r, g)]
@@ -208,6 +222,21 @@ int bqg_biqgemm_exact_f32(const void* d_keys, const float* d_alpha, const float*
 int bqg_biqgemm_exact_f64(const void* d_keys, const double* d_alpha, const double* d_x,
                           size_t x_rows, double* d_y, size_t m, size_t n, size_t b, unsigned beta,
                           unsigned mu, void* d_workspace, size_t workspace_bytes, void* stream);
+/* The same with the reference's KernelOptions::builder (kernel.hpp:51,158):
+ * BQG_LUT_DP or BQG_LUT_NAIVE (lut.hpp:31-43) -- y is bit-identical to the
+ * reference run with that builder.  stats (may be NULL) ACCUMULATES like
+ * KernelStats (kernel.hpp:197-202): the builder's op law, and the phase split
+ * of kernel.hpp:148-190 event-timed on `stream` (build = each group tile's
+ * LUT kernel, query = its lookup kernel, replace = accumulator zero-fill +
+ * alpha epilogue); with stats the call synchronises `stream`. */
+int bqg_biqgemm_exact_ex_f32(const void* d_keys, const float* d_alpha, const float* d_x, size_t x_rows,
+                             float* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                             int builder, void* d_workspace, size_t workspace_bytes,
+                             struct bqg_kernel_stats* stats, void* stream);
+int bqg_biqgemm_exact_ex_f64(const void* d_keys, const double* d_alpha, const double* d_x,
+                             size_t x_rows, double* d_y, size_t m, size_t n, size_t b, unsigned beta,
+                             unsigned mu, int builder, void* d_workspace, size_t workspace_bytes,
+                             struct bqg_kernel_stats* stats, void* stream);
 
 /* Comparison baselines on the GPU (reference baselines.hpp; not the BiQGEMM
  * path).  gemm_unpack (baselines.hpp:40-52): y = sum_i alpha_i * (B_i x)
@@ -226,13 +255,6 @@ int bqg_bandwidth_probe(const uint32_t* d_words, size_t m, size_t n, const float
  * workspace and a private stream: what the reference's callers hold. */
 typedef struct bqg_layer bqg_layer;
 
-typedef struct bqg_kernel_stats {
-    /* OpCounters (kernel.hpp:23-36), exact, computed analytically */
-    uint64_t lut_build_ops, lookups, accumulate_ops, fma_ops;
-    /* KernelStats phase seconds (kernel.hpp:41-46), CUDA-event timed:
-     * build+query = the fused kernel, replace = H2D of x + D2H of y */
-    double build_seconds, query_seconds, replace_seconds;
-} bqg_kernel_stats;
 
 /* quantize_greedy + pack_linear on the device from host weights W (m x n). */
 int bqg_layer_create_from_weights(const float* h_w, size_t m, size_t n, unsigned beta, unsigned mu,
@@ -259,7 +281,10 @@ const float* bqg_layer_device_alpha(const bqg_layer* layer);
 
 /* biqgemm(model, x) with HOST x (x_rows x b) and HOST y (m x b): H2D of x,
  * the fused kernel, D2H of y, synchronised before return -- the reference
- * call's contract.  exact != 0 selects the exact (fp64, bit-identical) path.
+ * call's contract.  exact selects the path: BQG_FORWARD_FAST (0), or the
+ * exact (fp64, bit-identical) path with the reference's Dp builder
+ * (BQG_FORWARD_EXACT, any nonzero value) or its Naive builder
+ * (BQG_FORWARD_EXACT_NAIVE; KernelOptions::builder, kernel.hpp:51,158).
  * stats (may be NULL) ACCUMULATES like KernelStats (kernel.hpp:197-202). */
 int bqg_layer_forward_host(bqg_layer* layer, const float* h_x, size_t x_rows, size_t b, float* h_y,
                            int exact, bqg_kernel_stats* stats);

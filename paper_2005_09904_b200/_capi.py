@@ -32,6 +32,9 @@ LUT_TABLE_MAJOR = 0
 LUT_KEY_MAJOR = 1
 LUT_DP = 0
 LUT_NAIVE = 1
+FORWARD_FAST = 0
+FORWARD_EXACT = 1
+FORWARD_EXACT_NAIVE = 2
 
 sz = C.c_size_t
 u32 = C.c_uint
@@ -106,6 +109,8 @@ SIGNATURES = {
     "bqg_biqgemm_exact_workspace_bytes": (sz, [sz, sz, sz, u32, u32]),
     "bqg_biqgemm_exact_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),
     "bqg_biqgemm_exact_f64": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, vp, sz, vp]),
+    "bqg_biqgemm_exact_ex_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, i32, vp, sz, P(KernelStats), vp]),
+    "bqg_biqgemm_exact_ex_f64": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, i32, vp, sz, P(KernelStats), vp]),
     "bqg_layer_create_from_weights": (i32, [vp, sz, sz, u32, u32, P(vp)]),
     "bqg_layer_create_from_device_weights": (i32, [vp, sz, sz, u32, u32, P(vp)]),
     "bqg_layer_create_from_keys": (i32, [vp, vp, sz, sz, u32, u32, P(vp)]),

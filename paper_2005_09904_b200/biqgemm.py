@@ -51,6 +51,36 @@ def _ptr(a) -> int:
     raise TypeError(type(a))
 
 
+def _check_buf(a, shape, where: str, name: str, device: bool):
+    """The C ABI takes raw pointers: a buffer of the wrong shape, dtype,
+    layout or memory space would be read / written out of bounds, so check
+    before the call (float32, C-contiguous, exact shape, host or device)."""
+    if torch is not None and isinstance(a, torch.Tensor):
+        ok_dtype, contig, on_dev = a.dtype == torch.float32, a.is_contiguous(), a.is_cuda
+    elif isinstance(a, np.ndarray):
+        ok_dtype, contig, on_dev = a.dtype == np.float32, a.flags["C_CONTIGUOUS"], False
+    else:
+        raise TypeError(f"{where}: {name} must be a numpy array or torch tensor, not {type(a).__name__}")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{where}: {name} has shape {tuple(a.shape)}, expected {tuple(shape)}")
+    if not ok_dtype:
+        raise TypeError(f"{where}: {name} must be float32")
+    if not contig:
+        raise ValueError(f"{where}: {name} must be C-contiguous")
+    if on_dev != device:
+        raise ValueError(f"{where}: {name} must be in {'device' if device else 'host'} memory")
+
+
+def _forward_path(exact: bool, builder: int) -> int:
+    """bqg_layer_forward_* path selector: KernelOptions::builder == Naive runs
+    the exact path with the reference's naive tables (kernel.hpp:51,158)."""
+    if builder == _capi.LUT_NAIVE:
+        return _capi.FORWARD_EXACT_NAIVE
+    if builder != _capi.LUT_DP:
+        raise ValueError(f"unknown LUT builder {builder}")
+    return _capi.FORWARD_EXACT if exact else _capi.FORWARD_FAST
+
+
 def _stream(stream=None):
     if stream is not None:
         return stream
@@ -346,25 +376,33 @@ class PackedLinear:
     def device_alpha(self) -> int:
         return lib.bqg_layer_device_alpha(self._h) or 0
 
-    def forward(self, x: np.ndarray, exact: bool = False, stats: KernelStats | None = None) -> np.ndarray:
-        """biqgemm(model, x): host x [x_rows, b] -> host y [m, b] (H2D + kernel + D2H)."""
+    def forward(self, x: np.ndarray, exact: bool = False, stats: KernelStats | None = None,
+                builder: int = _capi.LUT_DP) -> np.ndarray:
+        """biqgemm(model, x): host x [x_rows, b] -> host y [m, b] (H2D + kernel + D2H).
+        builder = LUT_NAIVE: the exact path with naive tables (KernelOptions::builder)."""
         x = np.ascontiguousarray(x, dtype=np.float32)
         if x.ndim == 1:
             x = x[:, None]
         y = np.empty((self.m, x.shape[1]), np.float32)
-        self.forward_into(x, y, exact=exact, stats=stats)
+        self.forward_into(x, y, exact=exact, stats=stats, builder=builder)
         return y
 
-    def forward_into(self, x, y, exact: bool = False, stats: KernelStats | None = None):
+    def forward_into(self, x, y, exact: bool = False, stats: KernelStats | None = None,
+                     builder: int = _capi.LUT_DP):
         """Host buffers (numpy or pinned torch CPU tensors) in and out."""
         x_rows, b = x.shape
-        check(lib.bqg_layer_forward_host(self._h, _ptr(x), x_rows, b, _ptr(y), 1 if exact else 0,
+        _check_buf(x, (x_rows, b), "forward_into", "x", device=False)
+        _check_buf(y, (self.m, b), "forward_into", "y", device=False)
+        check(lib.bqg_layer_forward_host(self._h, _ptr(x), x_rows, b, _ptr(y), _forward_path(exact, builder),
                                          C.byref(stats) if stats is not None else None))
         return y
 
-    def forward_device(self, x, y, exact: bool = False, pdl: bool = False, stream=None):
+    def forward_device(self, x, y, exact: bool = False, pdl: bool = False, stream=None,
+                       builder: int = _capi.LUT_DP):
         x_rows, b = x.shape
-        check(lib.bqg_layer_forward_device(self._h, _ptr(x), x_rows, b, _ptr(y), 1 if exact else 0,
+        _check_buf(x, (x_rows, b), "forward_device", "x", device=True)
+        _check_buf(y, (self.m, b), "forward_device", "y", device=True)
+        check(lib.bqg_layer_forward_device(self._h, _ptr(x), x_rows, b, _ptr(y), _forward_path(exact, builder),
                                            1 if pdl else 0, _stream(stream)))
         return y
 
@@ -388,6 +426,9 @@ def layers_forward_into(layers, x, y, exact: bool = False, stats: KernelStats | 
     torch CPU tensors).  The library pipelines H2D, the grouped kernels and
     D2H in sub-groups, synchronised.  `layers` is a list or a LayerGroup."""
     count, x_rows, b = x.shape
+    m = (layers.layers if isinstance(layers, LayerGroup) else layers)[0].m if count else 0
+    _check_buf(x, (count, x_rows, b), "layers_forward", "x", device=False)
+    _check_buf(y, (count, m, b), "layers_forward", "y", device=False)
     if isinstance(layers, LayerGroup):
         if len(layers) != count:
             raise ValueError(f"layers_forward: {len(layers)} layers for {count} inputs")
@@ -411,21 +452,22 @@ def pack_linear(w: np.ndarray, beta: int, mu: int) -> PackedLinear:
 
 
 def biqgemm(model: PackedLinear, x: np.ndarray, tile: TileShape | None = None, stats: KernelStats | None = None,
-            exact: bool = False) -> np.ndarray:
-    """biqgemm(model, x, tile, stats) (kernel.hpp:246-258).  The tile shape is
-    validated (t_w, t_h nonzero; kernel.hpp:135-137) but does not change the
-    result -- the reference guarantees that too (criterion 7)."""
+            exact: bool = False, builder: int = _capi.LUT_DP) -> np.ndarray:
+    """biqgemm(model, x, tile, stats, opts) (kernel.hpp:246-258).  The tile
+    shape is validated (t_w, t_h nonzero; kernel.hpp:135-137) but does not
+    change the result -- the reference guarantees that too (criterion 7).
+    builder is KernelOptions::builder (LUT_NAIVE: exact path, naive tables)."""
     if tile is not None and (tile.t_w == 0 or tile.t_h == 0):
         raise _capi.InvalidArgument(1, "biqgemm: tile dimensions must be nonzero")
-    return model.forward(x, exact=exact, stats=stats)
+    return model.forward(x, exact=exact, stats=stats, builder=builder)
 
 
 def biqgemm_plane(keys: np.ndarray, n: int, mu: int, x: np.ndarray, tile: TileShape | None = None,
-                  stats: KernelStats | None = None, exact: bool = False) -> np.ndarray:
+                  stats: KernelStats | None = None, exact: bool = False, builder: int = _capi.LUT_DP) -> np.ndarray:
     """biqgemm_plane (kernel.hpp:209-215): one key matrix [m, G], alpha = 1."""
     keys = np.asarray(keys)
     layer = PackedLinear.from_keys(keys[None, ...], None, n, mu)
     try:
-        return biqgemm(layer, x, tile, stats, exact)
+        return biqgemm(layer, x, tile, stats, exact, builder)
     finally:
         layer.close()

@@ -340,8 +340,9 @@ template <int MU, int BT>
 cudaError_t launch_cluster_mu_bt(const QueryParams& p, int cs, bool pdl, cudaStream_t stream, bool* used) {
     auto kern = biqgemm_cluster_kernel<MU, BT, kCNW, kCR>;
     const size_t smem = cluster_smem_bytes<MU, BT>();
-    static bool configured = false;
-    static int max_active[17] = {0};
+    static PerDeviceOnce configured;
+    static std::atomic<int> max_active[kMaxDevices][17];
+    const int dev = current_device();
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3((kCNW + 1) * 32);
     cfg.dynamicSmemBytes = smem;
@@ -355,29 +356,31 @@ cudaError_t launch_cluster_mu_bt(const QueryParams& p, int cs, bool pdl, cudaStr
     attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (!configured) {
+    cudaError_t ea = once_per_device(configured, dev, [&] {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    if (max_active[cs] == 0) {
+        return e;
+    });
+    if (ea != cudaSuccess) return ea;
+    int active = max_active[dev][cs].load(std::memory_order_relaxed);
+    if (active == 0) {  // occupancy of this cluster size on this device (racing threads compute the same answer)
         int n = 0;
         cfg.gridDim = dim3(static_cast<unsigned>(cs));
         if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
             cudaGetLastError();
             n = -1;
         }
-        max_active[cs] = n > 0 ? n : -1;
+        active = n > 0 ? n : -1;
+        max_active[dev][cs].store(active, std::memory_order_relaxed);
     }
-    if (max_active[cs] < 1) {
+    if (active < 1) {
         *used = false;
         return cudaSuccess;
     }
     ClusterPlan plan{};
     plan.cs = cs;
     plan.CT = (p.b + BT - 1) / BT;
-    plan.nclusters = std::min(max_active[cs], p.MT);
+    plan.nclusters = std::min(active, p.MT);
     plan.tq = p.MT / plan.nclusters;
     plan.tr = p.MT % plan.nclusters;
     {

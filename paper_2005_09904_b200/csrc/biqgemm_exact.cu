@@ -146,7 +146,10 @@ cudaError_t launch_build_lut_exact(const T* x, long long x_rows, long long b, in
 template <typename T>
 cudaError_t launch_biqgemm_exact(const void* keys, const T* alpha, const T* x, long long x_rows, T* y,
                                  long long m, long long n, int beta, int mu, long long b, void* workspace,
-                                 size_t workspace_bytes, cudaStream_t stream) {
+                                 size_t workspace_bytes, cudaStream_t stream, bool naive, const PhaseMarks* marks) {
+    auto mark = [&](int phase) {
+        if (marks) marks->mark(marks->ctx, phase, stream);
+    };
     if (workspace_bytes < exact_workspace_bytes(m, n, beta, mu, b)) return cudaErrorInvalidValue;
     const long long groups = (n + mu - 1) / mu;
     const size_t acc_bytes = static_cast<size_t>(beta) * m * b * sizeof(double);
@@ -157,8 +160,10 @@ cudaError_t launch_biqgemm_exact(const void* keys, const T* alpha, const T* x, l
     const long long tg = tile_groups(groups, mu, b);
     for (long long g0 = 0; g0 < groups; g0 += tg) {
         const long long count = std::min(tg, groups - g0);
-        e = launch_build_lut_exact<T>(x, x_rows, b, mu, g0, count, false, lut, stream);
+        mark(0);
+        e = launch_build_lut_exact<T>(x, x_rows, b, mu, g0, count, false, lut, stream, naive);
         if (e != cudaSuccess) return e;
+        mark(1);
         const long long work = static_cast<long long>(beta) * m * b;
         if (mu <= 8) {
             query_exact_kernel<uint8_t><<<blocks_for(work, 256), 256, 0, stream>>>(
@@ -170,6 +175,7 @@ cudaError_t launch_biqgemm_exact(const void* keys, const T* alpha, const T* x, l
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
+    mark(2);
     epilogue_exact_kernel<T><<<blocks_for(m * b, 256), 256, 0, stream>>>(acc, alpha, m, beta, b, y);
     return cudaGetLastError();
 }
@@ -180,9 +186,9 @@ template cudaError_t launch_build_lut_exact<double>(const double*, long long, lo
                                                     long long, bool, double*, cudaStream_t, bool);
 template cudaError_t launch_biqgemm_exact<float>(const void*, const float*, const float*, long long, float*,
                                                  long long, long long, int, int, long long, void*, size_t,
-                                                 cudaStream_t);
+                                                 cudaStream_t, bool, const PhaseMarks*);
 template cudaError_t launch_biqgemm_exact<double>(const void*, const double*, const double*, long long,
                                                   double*, long long, long long, int, int, long long, void*,
-                                                  size_t, cudaStream_t);
+                                                  size_t, cudaStream_t, bool, const PhaseMarks*);
 
 }  // namespace bqg

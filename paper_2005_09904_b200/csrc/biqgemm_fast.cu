@@ -353,12 +353,11 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     constexpr int R = stages_for<BT>();
     auto kern = biqgemm_fast_kernel<MU, BT, kNW, R>;
     const size_t smem = smem_bytes<MU, BT>();
-    static bool configured = false;  // one attribute call per instantiation
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce configured;  // one attribute call per instantiation and device
+    cudaError_t ea = once_per_device(configured, current_device(), [&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    });
+    if (ea != cudaSuccess) return ea;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(plan.grid));
     cfg.blockDim = dim3((kNW + 1) * 32);
@@ -494,12 +493,7 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
         const char* e = getenv("BQG_DEBUG_FLAGS");  // profiling switches; never set in production
         return e ? atoi(e) : 0;
     }();
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms(current_device());
     QueryParams p = p_in;
     p.debug = debug_flags;
     p.bt = pick_bt(p.b);

@@ -347,15 +347,21 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
 }
 
 template <int BETA>
-cudaError_t launch_lat_beta(const LatArgs& A, int nclusters, bool pdl, cudaStream_t stream) {
-    static bool configured = false;
-    auto kern = biqgemm_latency_kernel<BETA>;
-    if (!configured) {
+cudaError_t set_lat_attributes(int dev) {
+    static PerDeviceOnce configured;
+    return once_per_device(configured, dev, [] {
+        auto kern = biqgemm_latency_kernel<BETA>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLatSmem);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+        return e;
+    });
+}
+
+template <int BETA>
+cudaError_t launch_lat_beta(const LatArgs& A, int nclusters, bool pdl, cudaStream_t stream) {
+    auto kern = biqgemm_latency_kernel<BETA>;
+    cudaError_t ea = set_lat_attributes<BETA>(current_device());
+    if (ea != cudaSuccess) return ea;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(A.CS);
@@ -375,11 +381,13 @@ cudaError_t launch_lat_beta(const LatArgs& A, int nclusters, bool pdl, cudaStrea
 
 template <int BETA>
 int max_clusters(int cs) {
-    static int cache[17] = {0};
-    if (cache[cs] != 0) return cache[cs];
+    static std::atomic<int> cache[kMaxDevices][17];
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) return -1;
+    const int have = cache[dev][cs].load(std::memory_order_relaxed);
+    if (have != 0) return have;
     auto kern = biqgemm_latency_kernel<BETA>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLatSmem);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (set_lat_attributes<BETA>(dev) != cudaSuccess) return -1;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = static_cast<unsigned>(cs);
@@ -396,8 +404,9 @@ int max_clusters(int cs) {
         cudaGetLastError();
         n = -1;
     }
-    cache[cs] = n > 0 ? n : -1;
-    return cache[cs];
+    const int v = n > 0 ? n : -1;
+    cache[dev][cs].store(v, std::memory_order_relaxed);
+    return v;
 }
 
 }  // namespace

@@ -527,13 +527,12 @@ __global__ void __launch_bounds__(256) stream_finalize_kernel(const __grid_const
 
 template <int BETA>
 cudaError_t launch_stream_beta(const StreamArgs& A, bool pdl, cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(biqgemm_stream_kernel<BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kStreamSmem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce configured;
+    cudaError_t ea = once_per_device(configured, current_device(), [] {
+        return cudaFuncSetAttribute(biqgemm_stream_kernel<BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kStreamSmem);
+    });
+    if (ea != cudaSuccess) return ea;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
@@ -575,12 +574,7 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
     // this TMA-ring form, whose finaliser is a separate wide kernel.
     if (impl == 0 && count >= kTexMinGroup && tex_stream_applies(m, G, beta))
         return launch_biqgemm_tex(calls, count, x_rows, m, G, beta, ws, pdl, stream);
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = device_sms(current_device());
     StreamArgs A{};
     A.x_rows = x_rows;
     A.m = m;

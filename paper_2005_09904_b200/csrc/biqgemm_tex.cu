@@ -67,6 +67,12 @@ constexpr int kNWDefault = BQG_TEX_NW;   // gather warps (beta <= 3; fewer for b
 #ifndef BQG_TEX_NBW
 #define BQG_TEX_NBW 4
 #endif
+// L2 prefetch distance, in a warp's own unit strides (0 = off): when a warp
+// fetches unit u into registers it also asks L2 for unit u + PF*NW of the
+// same call (cp.async.bulk.prefetch, one lane), so the next fetches hit L2.
+#ifndef BQG_TEX_PF
+#define BQG_TEX_PF 0
+#endif
 constexpr int kNBW = BQG_TEX_NBW;   // builder warps (1, 2 or 4)
 template <int NW>
 struct TexGeom {
@@ -76,6 +82,27 @@ struct TexGeom {
 // memory is kept small on purpose: texture fetches in flight occupy L1
 // lines, and L1 is what the shared-memory carve-out leaves of 256 KiB.
 constexpr int kNL = 2;
+// Profiling switches, compile time (a variant build): 1 no LUT protocol,
+// 2 no gather, 4 no key fetch.
+#ifndef BQG_TEX_DBG
+#define BQG_TEX_DBG 0
+#endif
+constexpr int kTexDbg = BQG_TEX_DBG;
+// Builder warps poll for a free LUT buffer this often (a run lasts ~10 us at
+// C2; a poll is ~4 issue slots taken from the gather warps' SM sub-partition)
+constexpr unsigned kBuilderPollNs = 1000;
+#ifndef BQG_TEX_BPOLL
+#define BQG_TEX_BPOLL 1
+#endif
+#ifndef BQG_TEX_BFIRST
+#define BQG_TEX_BFIRST 1
+#endif
+__device__ __forceinline__ void builder_wait(uint64_t* bar, uint32_t parity) {
+    if (BQG_TEX_BPOLL)
+        mbar_wait_poll(bar, parity, kBuilderPollNs);
+    else
+        mbar_wait_sleep(bar, parity);
+}
 constexpr uint32_t kLutBase = 0x10000u;
 constexpr int kTexSmem = 0x20000;  // >= the end of the LUT region
 
@@ -93,10 +120,10 @@ struct TexArgs {
                              // window), so the handle is uniform: a handle picked with a per-warp
                              // index makes ptxas wrap each TLD in a waterfall loop that serialises
                              // the fetches (2.3 vs 6.4 TB/s, tools/ubench/tex_pattern.cu).
+    unsigned long long wbase[4];  // byte address of each window's first texel (L2 prefetch addresses)
     int ncalls;
     long long x_rows;
     int m, NB, MT, grid;
-    int dbg;  // profiling switches (BQG_TEX_DBG): 1 no LUT protocol, 2 no gather, 4 no key fetch
     long long total;  // ncalls * NB * MT units
     float* partial;   // ncalls x NB x (MT*32), fp32
     unsigned* cnt;    // [kStreamMaxGroup] completion counters (zero between launches)
@@ -273,28 +300,54 @@ __device__ __forceinline__ void advance(const TexArgs& A, Cursor& p, int by) {
     if (p.c != c0) load_call(A, p);
 }
 
+// Texel index of lane `lane`'s first 16 bytes of unit p (plane 0, low half).
 template <int BETA>
-__device__ __forceinline__ void fetch_unit(const TexArgs& A, const Cursor& p, int lane, Slot<BETA>& sl) {
-    const int base = p.toff + ((p.gb * A.MT + p.t) * BETA) * 64 + lane;
+__device__ __forceinline__ int unit_base(const TexArgs& A, const Cursor& p, int lane) {
+    return p.toff + ((p.gb * A.MT + p.t) * BETA) * 64 + lane;
+}
+
+// Plane i of a unit: the lane's two 16-byte pieces (bytes l*16 and 512 + l*16
+// of the plane's 1 KiB chunk).
+__device__ __forceinline__ void fetch_plane(const TexArgs& A, int win, int base, int i, uint4 (&k)[2]) {
     auto fetch = [&](cudaTextureObject_t tex) {
-#pragma unroll
-        for (int i = 0; i < BETA; ++i) {
-            sl.k[i][0] = tex1Dfetch<uint4>(tex, base + i * 64);
-            sl.k[i][1] = tex1Dfetch<uint4>(tex, base + i * 64 + 32);
-        }
+        k[0] = tex1Dfetch<uint4>(tex, base + i * 64);
+        k[1] = tex1Dfetch<uint4>(tex, base + i * 64 + 32);
     };
-    switch (p.win) {  // warp-uniform branch, constant-index (uniform) handle in each arm
+    switch (win) {  // warp-uniform branch, constant-index (uniform) handle in each arm
         case 0: fetch(A.tex[0]); break;
         case 1: fetch(A.tex[1]); break;
         case 2: fetch(A.tex[2]); break;
         default: fetch(A.tex[3]); break;
     }
+}
+
+// Everything of a unit but its keys: alpha, partial index, run; and the
+// optional L2 prefetch of a unit further ahead.
+template <int BETA, int NW>
+__device__ __forceinline__ void unit_meta(const TexArgs& A, const Cursor& p, int lane, float (&a)[BETA],
+                                          uint32_t& pidx, int& q) {
+#if BQG_TEX_PF > 0
+    const int uic = p.gb * A.MT + p.t;  // unit index inside the call
+    if (lane == 0 && uic + BQG_TEX_PF * NW < A.NB * A.MT) {
+        const unsigned long long addr =
+            A.wbase[p.win] + 16ull * static_cast<unsigned long long>(p.toff + ((uic + BQG_TEX_PF * NW) * BETA) * 64);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(addr), "r"(BETA * 1024) : "memory");
+    }
+#endif
     const int r = p.t * 32 + lane;
 #pragma unroll
     for (int i = 0; i < BETA; ++i)
-        sl.a[i] = r < A.m ? (p.al ? __ldg(p.al + static_cast<long long>(i) * A.m + r) : 1.0f) : 0.0f;
-    sl.pidx = r < A.m ? static_cast<uint32_t>((p.c * A.NB + p.gb) * A.MT) * 32u + static_cast<uint32_t>(r) : ~0u;
-    sl.q = p.q;
+        a[i] = r < A.m ? (p.al ? __ldg(p.al + static_cast<long long>(i) * A.m + r) : 1.0f) : 0.0f;
+    pidx = r < A.m ? static_cast<uint32_t>((p.c * A.NB + p.gb) * A.MT) * 32u + static_cast<uint32_t>(r) : ~0u;
+    q = p.q;
+}
+
+template <int BETA, int NW>
+__device__ __forceinline__ void fetch_unit(const TexArgs& A, const Cursor& p, int lane, Slot<BETA>& sl) {
+    const int base = unit_base<BETA>(A, p, lane);
+#pragma unroll
+    for (int i = 0; i < BETA; ++i) fetch_plane(A, p.win, base, i, sl.k[i]);
+    unit_meta<BETA, NW>(A, p, lane, sl.a, sl.pidx, sl.q);
 }
 
 __device__ __forceinline__ int ld_volatile_s32(const int* p) {
@@ -402,7 +455,7 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
     if (warp >= kNW) {
         // ------------------------------------------------ builders
         const int which = warp - kNW;
-        if (A.dbg & 1) return;
+        if (kTexDbg & 1) return;
         // Run q's gather is complete (its ldone phase): if it is the CTA's
         // last run of call c, add the CTA's unit count of c to c's counter;
         // the CTA that completes the count owns y_c's finalisation.
@@ -445,20 +498,31 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
                 for (int t = 0; t < kMU; ++t) xv[t] = r0 + t < A.x_rows ? __ldg(x + r0 + t) : 0.0f;
             }
             const int buf = q % kNL;
+            // LUT buffer `buf` is free once run q - kNL is gathered; the gather
+            // warps are then on run q - 1, which lasts far longer than a poll
+            if (q >= kNL) builder_wait(&ldone[buf], static_cast<uint32_t>((q / kNL - 1) & 1));
+#if !BQG_TEX_BFIRST
             if (q >= kNL) {
-                mbar_wait_sleep(&ldone[buf], static_cast<uint32_t>((q / kNL - 1) & 1));
                 signal_run(q - kNL);
-                named_bar_sync(1, kNBW * 32);  // every builder sees a task posted just now
-                fin_drain(A, fq, tcur, lane);  // builders finalise while the gather warps run on
+                named_bar_sync(1, kNBW * 32);
+                fin_drain(A, fq, tcur, lane);
             }
+#endif
             build_tables_reg<kNBW>(which,
                                    lut_abs + static_cast<uint32_t>(buf >> 1) * 0x10000u +
                                        static_cast<uint32_t>(buf & 1) * 128u + static_cast<uint32_t>(lane) * 4u,
                                    xv);
             mbar_arrive(&lfull[buf]);
+            // only then signal run q - kNL and finalise what became ready: a
+            // finalisation (up to a whole call) must never delay a LUT
+            if (BQG_TEX_BFIRST && q >= kNL) {
+                signal_run(q - kNL);
+                named_bar_sync(1, kNBW * 32);  // every builder sees a task posted just now
+                fin_drain(A, fq, tcur, lane);  // builders finalise while the gather warps run on
+            }
         }
         for (int q = max(0, nruns - kNL); q < nruns; ++q) {
-            mbar_wait_sleep(&ldone[q % kNL], static_cast<uint32_t>((q / kNL) & 1));
+            builder_wait(&ldone[q % kNL], static_cast<uint32_t>((q / kNL) & 1));
             signal_run(q);
         }
         named_bar_sync(1, kNBW * 32);
@@ -489,13 +553,6 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
         pf.gb = static_cast<int>(cb - static_cast<long long>(pf.c) * A.NB);
         load_call(A, pf);
     }
-    Slot<BETA> S[UD];
-#pragma unroll
-    for (int d = 0; d < UD; ++d) {
-        if (d < nk) fetch_unit<BETA>(A, pf, lane, S[d]);
-        advance(A, pf, kNW);
-    }
-    pdl_wait();  // the previous launch may still read the partials / counters
     // Every warp walks EVERY run of the CTA in order -- wait LUT(q) built,
     // gather its units of run q (maybe none), release run q -- so a release
     // of run q + kNL always follows the build of run q + kNL, which follows
@@ -509,13 +566,28 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
             mbar_wait(&lfull[cur % kNL], static_cast<uint32_t>((cur / kNL) & 1));
         }
     };
+    auto store_partial = [&](uint32_t pidx, double s) {
+        if (pidx != ~0u) {
+            // partials stay in L2 for the finaliser (L2 evict_last)
+            asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(A.partial + pidx),
+                         "f"(static_cast<float>(s)), "l"(pol_keep)
+                         : "memory");
+        }
+    };
+    Slot<BETA> S[UD];
+#pragma unroll
+    for (int d = 0; d < UD; ++d) {
+        if (d < nk) fetch_unit<BETA, kNW>(A, pf, lane, S[d]);
+        advance(A, pf, kNW);
+    }
+    pdl_wait();  // the previous launch may still read the partials / counters
     for (int k0 = 0; k0 < nk; k0 += UD) {
 #pragma unroll
         for (int d = 0; d < UD; ++d) {
             if (k0 + d < nk) {
-                if (!(A.dbg & 1)) move_to(S[d].q);
+                if (!(kTexDbg & 1)) move_to(S[d].q);
                 double s;
-                if (A.dbg & 2) {
+                if (kTexDbg & 2) {
                     uint32_t h = 0;
 #pragma unroll
                     for (int i = 0; i < BETA; ++i) h ^= S[d].k[i][0].x ^ S[d].k[i][0].y ^ S[d].k[i][1].z ^ S[d].k[i][1].w;
@@ -526,35 +598,28 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
                     s = tex_unit<BETA, kLutBase + 128>(S[d].k, S[d].a, rot);
                 }
                 const uint32_t pidx = S[d].pidx;
-                if (k0 + d + UD < nk && !(A.dbg & 4)) fetch_unit<BETA>(A, pf, lane, S[d]);
+                if (k0 + d + UD < nk && !(kTexDbg & 4)) fetch_unit<BETA, kNW>(A, pf, lane, S[d]);
                 advance(A, pf, kNW);
-                if (pidx != ~0u) {
-                    // partials stay in L2 for the finaliser (L2 evict_last)
-                    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(A.partial + pidx),
-                                 "f"(static_cast<float>(s)), "l"(pol_keep)
-                                 : "memory");
-                }
+                store_partial(pidx, s);
             }
         }
     }
-    if (A.dbg & 1) return;
+    if (kTexDbg & 1) return;
     move_to(nruns - 1);
     mbar_arrive(&ldone[cur % kNL]);
-    mbar_wait_sleep(fbar, 0);      // the CTA's last tasks are posted: everyone helps finish them
+    mbar_wait_poll(fbar, 0, 256);  // the CTA's last tasks are posted: everyone helps finish them
     fin_drain(A, fq, tcur, lane);
 }
 
 // Per-device caches (cudaFuncSetAttribute and the SM count are per device).
-constexpr int kMaxDev = 64;
-std::once_flag g_attr_once[kMaxDev][4];
-int g_sms[kMaxDev];
-std::once_flag g_sms_once[kMaxDev];
+constexpr int kMaxDev = kMaxDevices;
 
 template <int BETA, int UD, int NW>
 cudaError_t launch_tex_beta(const TexArgs& A, int dev, bool pdl, cudaStream_t stream) {
-    cudaError_t ea = cudaSuccess;
-    std::call_once(g_attr_once[dev][BETA - 1], [&] {
-        ea = cudaFuncSetAttribute(biqgemm_tex_kernel<BETA, UD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTexSmem);
+    static PerDeviceOnce configured;
+    const cudaError_t ea = once_per_device(configured, dev, [] {
+        return cudaFuncSetAttribute(biqgemm_tex_kernel<BETA, UD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kTexSmem);
     });
     if (ea != cudaSuccess) return ea;
     cudaLaunchAttribute attr[1];
@@ -651,7 +716,6 @@ cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_r
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
-    std::call_once(g_sms_once[dev], [&] { cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev); });
     std::vector<TexArgs> buf(1);  // ~12 KiB: keep it off the caller's stack
     TexArgs& A = buf[0];
     A.x_rows = x_rows;
@@ -677,11 +741,7 @@ cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_r
         }
     }
     A.partial = ws + kTexCounterBytes / sizeof(float);
-    static const int dbg = [] {
-        const char* v = getenv("BQG_TEX_DBG");
-        return v ? atoi(v) : 0;
-    }();
-    A.dbg = dbg;
+    static const bool verbose = getenv("BQG_TEX_VERBOSE") != nullptr;
     const size_t key_bytes = static_cast<size_t>(A.NB) * A.MT * beta * 1024;
     const long long texels = max_texels(dev);
     // Address windows: greedy over the calls' key buffers sorted by address,
@@ -731,11 +791,12 @@ cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_r
                 if (e != cudaSuccess) return e;
             }
             A.tex[k] = static_cast<unsigned long long>(t);
+            A.wbase[k] = k < nw ? static_cast<unsigned long long>(wins[slot_of_win[k]].first) : 0ull;
         }
         A.ncalls = n;
-        if (dbg & 16) fprintf(stderr, "[bqg tex] launch of %d calls, %d windows\n", n, nw);
+        if (verbose) fprintf(stderr, "[bqg tex] launch of %d calls, %d windows\n", n, nw);
         A.total = static_cast<long long>(A.ncalls) * A.NB * A.MT;
-        A.grid = static_cast<int>(std::min<long long>(g_sms[dev], A.total));
+        A.grid = static_cast<int>(std::min<long long>(device_sms(dev), A.total));
         const bool p = pdl || done > 0;
         switch (beta) {
             case 1: e = launch_tex_beta<1, 3, kNWDefault>(A, dev, p, stream); break;

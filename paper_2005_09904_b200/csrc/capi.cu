@@ -552,10 +552,47 @@ extern "C" size_t bqg_biqgemm_exact_workspace_bytes(size_t m, size_t n, size_t b
                                       static_cast<int>(mu), static_cast<long long>(b));
 }
 
+namespace {
+// Event trail of one exact call: an event before the call, one per phase
+// mark (bqg::PhaseMarks), one after.  The reference's phase split
+// (kernel.hpp:156-159): build = each tile's LUT build, query = each tile's
+// lookups, replace = accumulator setup + the alpha epilogue.
+struct EventTrail {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> phase;
+    cudaError_t err = cudaSuccess;
+    static void mark(void* ctx, int ph, cudaStream_t s) {
+        auto* t = static_cast<EventTrail*>(ctx);
+        cudaEvent_t e = nullptr;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r == cudaSuccess) r = cudaEventRecord(e, s);
+        if (r != cudaSuccess) {
+            if (t->err == cudaSuccess) t->err = r;
+            if (e) cudaEventDestroy(e);
+            return;
+        }
+        t->ev.push_back(e);
+        t->phase.push_back(ph);
+    }
+    ~EventTrail() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+    // seconds[0..2] += build, query, replace
+    void accumulate(double* seconds) const {
+        for (size_t i = 0; i + 1 < ev.size(); ++i) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            const int ph = phase[i];
+            seconds[ph == 0 ? 0 : (ph == 1 ? 1 : 2)] += ms * 1e-3;
+        }
+    }
+};
+}  // namespace
+
 template <typename T>
 static int biqgemm_exact_impl(const void* d_keys, const T* d_alpha, const T* d_x, size_t x_rows, T* d_y, size_t m,
-                              size_t n, size_t b, unsigned beta, unsigned mu, void* d_ws, size_t ws_bytes,
-                              void* stream) {
+                              size_t n, size_t b, unsigned beta, unsigned mu, int builder, void* d_ws,
+                              size_t ws_bytes, bqg_kernel_stats* stats, void* stream) {
     int s = check_mu(mu, "biqgemm");
     if (s) return s;
     s = check_dims(m, n, "biqgemm");
@@ -564,27 +601,68 @@ static int biqgemm_exact_impl(const void* d_keys, const T* d_alpha, const T* d_x
     s = check_x(x_rows, b, n, mu, "biqgemm");
     if (s) return s;
     if (!d_keys || !d_x || !d_y || !d_ws) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: null pointer");
+    if (builder != BQG_LUT_DP && builder != BQG_LUT_NAIVE)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: unsupported builder");
     if (ws_bytes < bqg_biqgemm_exact_workspace_bytes(m, n, b, beta, mu))
         return set_err(BQG_ERR_WORKSPACE, "biqgemm_exact: workspace too small");
     BQG_NEED_DEVICE();
+    cudaStream_t st = as_stream(stream);
+    EventTrail trail;
+    const bqg::PhaseMarks marks{&trail, &EventTrail::mark};
+    if (stats) EventTrail::mark(&trail, 2, st);  // accumulator zero-fill: "replace" (kernel.hpp:148-150)
     cudaError_t e = bqg::launch_biqgemm_exact<T>(d_keys, d_alpha, d_x, static_cast<long long>(x_rows), d_y,
                                                  static_cast<long long>(m), static_cast<long long>(n),
                                                  static_cast<int>(beta), static_cast<int>(mu),
-                                                 static_cast<long long>(b), d_ws, ws_bytes, as_stream(stream));
+                                                 static_cast<long long>(b), d_ws, ws_bytes, st,
+                                                 builder == BQG_LUT_NAIVE, stats ? &marks : nullptr);
     if (e != cudaSuccess) return cuda_err(e, "biqgemm exact kernels");
+    if (stats) {
+        EventTrail::mark(&trail, 3, st);
+        if (trail.err != cudaSuccess) return cuda_err(trail.err, "biqgemm exact: phase events");
+        BQG_CUDA(cudaStreamSynchronize(st));
+        uint64_t ops[4];
+        bqg_op_counters(m, n, b, beta, mu, builder, ops);
+        stats->lut_build_ops += ops[0];
+        stats->lookups += ops[1];
+        stats->accumulate_ops += ops[2];
+        stats->fma_ops += ops[3];
+        double sec[3] = {0.0, 0.0, 0.0};
+        trail.accumulate(sec);
+        stats->build_seconds += sec[0];
+        stats->query_seconds += sec[1];
+        stats->replace_seconds += sec[2];
+    }
     return BQG_OK;
 }
 
 extern "C" int bqg_biqgemm_exact_f32(const void* d_keys, const float* d_alpha, const float* d_x, size_t x_rows,
                                      float* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
                                      void* d_ws, size_t ws_bytes, void* stream) {
-    return biqgemm_exact_impl<float>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, d_ws, ws_bytes, stream);
+    return biqgemm_exact_impl<float>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, BQG_LUT_DP, d_ws,
+                                     ws_bytes, nullptr, stream);
 }
 
 extern "C" int bqg_biqgemm_exact_f64(const void* d_keys, const double* d_alpha, const double* d_x, size_t x_rows,
                                      double* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
                                      void* d_ws, size_t ws_bytes, void* stream) {
-    return biqgemm_exact_impl<double>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, d_ws, ws_bytes, stream);
+    return biqgemm_exact_impl<double>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, BQG_LUT_DP, d_ws,
+                                      ws_bytes, nullptr, stream);
+}
+
+extern "C" int bqg_biqgemm_exact_ex_f32(const void* d_keys, const float* d_alpha, const float* d_x, size_t x_rows,
+                                        float* d_y, size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                        int builder, void* d_ws, size_t ws_bytes, bqg_kernel_stats* stats,
+                                        void* stream) {
+    return biqgemm_exact_impl<float>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, builder, d_ws, ws_bytes,
+                                     stats, stream);
+}
+
+extern "C" int bqg_biqgemm_exact_ex_f64(const void* d_keys, const double* d_alpha, const double* d_x,
+                                        size_t x_rows, double* d_y, size_t m, size_t n, size_t b, unsigned beta,
+                                        unsigned mu, int builder, void* d_ws, size_t ws_bytes,
+                                        bqg_kernel_stats* stats, void* stream) {
+    return biqgemm_exact_impl<double>(d_keys, d_alpha, d_x, x_rows, d_y, m, n, b, beta, mu, builder, d_ws,
+                                      ws_bytes, stats, stream);
 }
 
 // ============================================================== comparison baselines
@@ -866,15 +944,20 @@ extern "C" const float* bqg_layer_device_alpha(const bqg_layer* L) { return L ? 
 
 namespace {
 
+// exact: BQG_FORWARD_FAST (0), BQG_FORWARD_EXACT (fp64 DP tables) or
+// BQG_FORWARD_EXACT_NAIVE (fp64 naive tables: KernelOptions::builder = Naive,
+// kernel.hpp:51,158).  xstats (exact path only) receives the exact path's
+// counters and build/query/replace split; it synchronises the stream.
 int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float* d_y, int exact, int pdl,
-                  cudaStream_t st) {
+                  cudaStream_t st, bqg_kernel_stats* xstats = nullptr) {
     if (exact || L->mu > 8) {
         const size_t need = bqg_biqgemm_exact_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
         if (need > L->ws_exact_bytes) ++L->buf_gen;
         int s = grow(L->d_ws_exact, L->ws_exact_bytes, need);
         if (s) return s;
-        return bqg_biqgemm_exact_f32(L->d_keys, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu,
-                                     L->d_ws_exact, L->ws_exact_bytes, st);
+        return biqgemm_exact_impl<float>(L->d_keys, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu,
+                                         exact == BQG_FORWARD_EXACT_NAIVE ? BQG_LUT_NAIVE : BQG_LUT_DP,
+                                         L->d_ws_exact, L->ws_exact_bytes, xstats, st);
     }
     const size_t need = bqg_biqgemm_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
     if (need > L->ws_bytes) {
@@ -999,7 +1082,9 @@ extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_r
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[0], st));
     BQG_CUDA(cudaMemcpyAsync(L->d_x, xpin ? h_x : L->h_x_pin, xbytes, cudaMemcpyHostToDevice, st));
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[1], st));
-    s = layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st);
+    const bool exact_path = exact || L->mu > 8;
+    bqg_kernel_stats xs{};
+    s = layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st, exact_path ? &xs : nullptr);
     if (s) return s;
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[2], st));
     BQG_CUDA(cudaMemcpyAsync(ypin ? h_y : L->h_y_pin, L->d_y, ybytes, cudaMemcpyDeviceToHost, st));
@@ -1007,17 +1092,30 @@ extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_r
     BQG_CUDA(cudaStreamSynchronize(st));
     if (!ypin) std::memcpy(h_y, L->h_y_pin, ybytes);
     if (stats) {
-        uint64_t ops[4];
-        bqg_op_counters(L->m, L->n, b, L->beta, L->mu, BQG_LUT_DP, ops);
-        stats->lut_build_ops += ops[0];
-        stats->lookups += ops[1];
-        stats->accumulate_ops += ops[2];
-        stats->fma_ops += ops[3];
         float t01 = 0, t12 = 0, t23 = 0;
         cudaEventElapsedTime(&t01, L->ev[0], L->ev[1]);
         cudaEventElapsedTime(&t12, L->ev[1], L->ev[2]);
         cudaEventElapsedTime(&t23, L->ev[2], L->ev[3]);
-        stats->query_seconds += t12 * 1e-3;
+        if (exact_path) {
+            // separate build / query kernels: the reference's phase split
+            stats->lut_build_ops += xs.lut_build_ops;
+            stats->lookups += xs.lookups;
+            stats->accumulate_ops += xs.accumulate_ops;
+            stats->fma_ops += xs.fma_ops;
+            stats->build_seconds += xs.build_seconds;
+            stats->query_seconds += xs.query_seconds;
+            stats->replace_seconds += xs.replace_seconds;
+        } else {
+            // fast path: the LUT build runs inside the query kernel (builder
+            // warps overlap the gather), so its time is part of query_seconds
+            uint64_t ops[4];
+            bqg_op_counters(L->m, L->n, b, L->beta, L->mu, BQG_LUT_DP, ops);
+            stats->lut_build_ops += ops[0];
+            stats->lookups += ops[1];
+            stats->accumulate_ops += ops[2];
+            stats->fma_ops += ops[3];
+            stats->query_seconds += t12 * 1e-3;
+        }
         stats->replace_seconds += (t01 + t23) * 1e-3;
     }
     return BQG_OK;
@@ -1135,32 +1233,46 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
     std::vector<bqg_call> calls(count);
     for (size_t i = 0; i < count; ++i) calls[i] = {layers[i]->d_tiled, layers[i]->d_alpha, G.d_x + i * xs, G.d_y + i * ys};
     cudaStream_t st = G.stream, cp = G.copy, dp = G.down;
-    if (stats) BQG_CUDA(cudaEventRecord(G.ev[0], cp));
-    // all H2D copies are queued first (the copy stream runs ahead of the kernels)
-    for (size_t k = 0; k < nsub; ++k) {
-        const size_t i0 = starts[k], cnt = starts[k + 1] - i0;
-        BQG_CUDA(cudaMemcpyAsync(G.d_x + i0 * xs, h_x + i0 * xs, sizeof(float) * xs * cnt, cudaMemcpyHostToDevice, cp));
-        BQG_CUDA(cudaEventRecord(G.chunk_ev[2 * k], cp));
+    // Everything below queues asynchronous work that reads h_x and writes
+    // h_y.  On an error part-way, the copies already queued must land before
+    // control returns: the caller may free or reuse its host buffers (and the
+    // next call may regrow G.d_x / G.d_y) as soon as we return.
+    auto pipeline = [&]() -> int {
+        if (stats) BQG_CUDA(cudaEventRecord(G.ev[0], cp));
+        // all H2D copies are queued first (the copy stream runs ahead of the kernels)
+        for (size_t k = 0; k < nsub; ++k) {
+            const size_t i0 = starts[k], cnt = starts[k + 1] - i0;
+            BQG_CUDA(cudaMemcpyAsync(G.d_x + i0 * xs, h_x + i0 * xs, sizeof(float) * xs * cnt, cudaMemcpyHostToDevice, cp));
+            BQG_CUDA(cudaEventRecord(G.chunk_ev[2 * k], cp));
+        }
+        for (size_t k = 0; k < nsub; ++k) {
+            const size_t i0 = starts[k], cnt = starts[k + 1] - i0;
+            cudaEvent_t h2d = G.chunk_ev[2 * k], done = G.chunk_ev[2 * k + 1];
+            BQG_CUDA(cudaStreamWaitEvent(st, h2d, 0));
+            if (stats && k == 0) BQG_CUDA(cudaEventRecord(G.ev[1], st));
+            s = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap,
+                                        k > 0 ? 1 : 0, st);
+            if (s) return s;
+            BQG_CUDA(cudaEventRecord(done, st));
+            BQG_CUDA(cudaStreamWaitEvent(dp, done, 0));
+            BQG_CUDA(cudaMemcpyAsync(h_y + i0 * ys, G.d_y + i0 * ys, sizeof(float) * ys * cnt, cudaMemcpyDeviceToHost, dp));
+        }
+        if (stats) {
+            BQG_CUDA(cudaEventRecord(G.ev[2], st));
+            BQG_CUDA(cudaEventRecord(G.ev[3], dp));
+        }
+        BQG_CUDA(cudaStreamSynchronize(dp));
+        BQG_CUDA(cudaStreamSynchronize(st));
+        BQG_CUDA(cudaStreamSynchronize(cp));
+        return BQG_OK;
+    };
+    s = pipeline();
+    if (s) {
+        cudaStreamSynchronize(cp);  // drain whatever was queued (status ignored: s is the error reported)
+        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(dp);
+        return s;
     }
-    for (size_t k = 0; k < nsub; ++k) {
-        const size_t i0 = starts[k], cnt = starts[k + 1] - i0;
-        cudaEvent_t h2d = G.chunk_ev[2 * k], done = G.chunk_ev[2 * k + 1];
-        BQG_CUDA(cudaStreamWaitEvent(st, h2d, 0));
-        if (stats && k == 0) BQG_CUDA(cudaEventRecord(G.ev[1], st));
-        s = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, L0->n, b, L0->beta, L0->mu, G.d_ws, G.ws_cap,
-                                    k > 0 ? 1 : 0, st);
-        if (s) return s;
-        BQG_CUDA(cudaEventRecord(done, st));
-        BQG_CUDA(cudaStreamWaitEvent(dp, done, 0));
-        BQG_CUDA(cudaMemcpyAsync(h_y + i0 * ys, G.d_y + i0 * ys, sizeof(float) * ys * cnt, cudaMemcpyDeviceToHost, dp));
-    }
-    if (stats) {
-        BQG_CUDA(cudaEventRecord(G.ev[2], st));
-        BQG_CUDA(cudaEventRecord(G.ev[3], dp));
-    }
-    BQG_CUDA(cudaStreamSynchronize(dp));
-    BQG_CUDA(cudaStreamSynchronize(st));
-    BQG_CUDA(cudaStreamSynchronize(cp));
     if (stats) {
         uint64_t ops[4];
         bqg_op_counters(L0->m, L0->n, b, L0->beta, L0->mu, BQG_LUT_DP, ops);

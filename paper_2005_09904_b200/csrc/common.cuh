@@ -4,7 +4,45 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 namespace bqg {
+
+// ---- host-side per-device launch state ---------------------------------------
+
+// Kernel attributes (cudaFuncSetAttribute), occupancy answers and the SM
+// count belong to a DEVICE, not to the process: a process that drives two
+// GPUs must configure each one.  Every launcher keeps its one-time state in
+// a PerDevice table indexed by the current device ordinal, initialised under
+// std::call_once (thread-safe).
+constexpr int kMaxDevices = 64;
+struct PerDeviceOnce {
+    std::once_flag flag[kMaxDevices];
+    cudaError_t err[kMaxDevices] = {};
+};
+inline int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return -1;
+    return d;
+}
+// Runs f() once per device; later calls return f()'s first result.
+template <class F>
+inline cudaError_t once_per_device(PerDeviceOnce& o, int dev, F&& f) {
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::call_once(o.flag[dev], [&] { o.err[dev] = f(); });
+    return o.err[dev];
+}
+inline int device_sms(int dev) {
+    static std::atomic<int> sms[kMaxDevices];
+    if (dev < 0 || dev >= kMaxDevices) return 148;
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sms[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
 
 // ---- launch-level helpers ---------------------------------------------------
 
@@ -137,7 +175,15 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// Same, but the thread may sleep until the phase completes (suspend-time
+// Wait by polling with a fixed sleep between tests: for warps that wait a
+// long time (many microseconds) off the critical path.  Each poll costs ~4
+// issue slots; the hardware-suspended try_wait of mbar_wait_sleep (below)
+// wakes far more often than that (measured: ~10 polls per gathered unit in
+// the texture form).
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* bar, uint32_t parity, unsigned sleep_ns) {
+    while (!mbar_test(bar, parity)) __nanosleep(sleep_ns);
+}
+// Like mbar_wait, but the thread may sleep until the phase completes (suspend-time
 // hint): for warps that wait long (producers, builders, loaders) so that
 // their retries do not take issue slots from the gather warps.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {

@@ -112,11 +112,20 @@ template <typename T>
 cudaError_t launch_build_lut_exact(const T* x, long long x_rows, long long b, int mu, long long g0,
                                    long long count, bool key_major, double* out,
                                    cudaStream_t stream, bool naive = false);
+// Phase marks for KernelStats (kernel.hpp:41-46,156-159): mark(ctx, phase)
+// is called on the host right before the launches of each phase are queued
+// (phase 0 = a tile's LUT build, 1 = its query, 2 = the alpha epilogue), so
+// the caller can record an event on the stream there.
+struct PhaseMarks {
+    void* ctx;
+    void (*mark)(void* ctx, int phase, cudaStream_t stream);
+};
 template <typename T>
 cudaError_t launch_biqgemm_exact(const void* keys_rowmajor, const T* alpha, const T* x,
                                  long long x_rows, T* y, long long m, long long n, int beta,
                                  int mu, long long b, void* workspace, size_t workspace_bytes,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, bool naive = false,
+                                 const PhaseMarks* marks = nullptr);
 size_t exact_workspace_bytes(long long m, long long n, int beta, int mu, long long b);
 
 }  // namespace bqg
