@@ -4,42 +4,51 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
 
 Workload (N=1): BASELINE.json configs[1] = C2, the metric's own config:
-GEMV m=n=4096, q(beta)=3 binary planes, mu=8, batch b=1, inputs generated
+GEMV m=n=4096, q(beta)=3 binary planes, mu=8, batch b=1, weights generated
 exactly like the reference's bench_cli (W = random_uniform(m,n,0x5EED),
-x = random_normal(n,b,0x5EED+1)), quantized + packed ON THE GPU by the
-product path.  A "step" is one BiQGEMM call (fused LUT build -> LUT query
--> alpha scale) on one layer's weights.
+x = random_normal(n,b,0x5EED+1+j)), quantized + packed ON THE GPU by the
+product path.
 
-Timing (device, `value`): the K timed calls are independent (each its own
-weight copy, its own x, its own LUT build and y) and are issued through the
-grouped C-ABI entry, G = 128 calls per launch (bqg_biqgemm_grouped_f32: one
-persistent kernel whose key stream runs ahead across call boundaries, then a
-fixed-order epilogue kernel), captured in one CUDA graph and replayed once
-between a barrier+synchronize pair, timed with CUDA events on the replay
-stream.  Calls rotate over R distinct weight copies totalling > 2x the 126 MB
-L2, so every call streams its packed keys from HBM (inputs larger than L2; no
-flush needed).  value = packed-key bytes of all ranks / max-over-ranks time,
-in GB/s; us/call is reported beside it.
+A STEP (b = 1 configs) is one grouped launch of G = 128 independent BiQGEMM
+calls -- a serving batch / the projections of a layer stack: every call has
+its own weight copy, its own x, its own LUT build and its own y, issued
+through the grouped C-ABI entry (bqg_biqgemm_grouped_f32, one persistent
+kernel per launch).  `--steps K` times exactly K such launches (K*G calls),
+captured in one CUDA graph and replayed between barrier+synchronize pairs,
+CUDA events on the replay stream, median of >= 3 replays.  Calls rotate over
+R distinct weight copies totalling > 2x the 126 MB L2, so every call streams
+its packed keys from HBM whatever K is (inputs larger than L2; no flush).
+value = packed-key bytes of all ranks / max-over-ranks time, in GB/s;
+us/call and the roofline fraction are reported beside it.  For b > 1 configs
+(C3, C5) a step is one call (its own weight copy).
 
-`latency`: the dependent-call regime -- one single-call kernel per step,
-each PDL-chained behind its predecessor (consecutive layers of one model).
+`latency`: the dependent-call regime -- 512 single-call kernels, each
+PDL-chained behind its predecessor (consecutive layers of one model).
+`group_sweep`: us/call for G = 1, 3, 8, 32, 128, 512 calls per launch.
 
 e2e: the same calls through the public C ABI with HOST buffers
-(bqg_layers_forward_host per 512 calls: H2D of the inputs from pinned
-memory, the grouped kernels, D2H of the outputs -- pipelined inside the call
-in sub-groups sized by host I/O (C2: 64, 128, 256 ... 128, 64 calls) --
-synchronised), wall-clock timed.
+(bqg_layers_forward_host, one synchronised API call per step of G calls: H2D
+of the inputs from pinned memory, the grouped kernels, D2H of the outputs,
+pipelined inside the call), wall-clock timed.
 
-N>1 (torchrun): weak scaling -- every rank owns a C2-sized row shard of an
-(N*4096) x 4096 layer, and y is assembled with an NCCL all-gather each step.
+N>1 (torchrun, one GPU per rank, NCCL): the north-star decomposition through
+the sharded C-ABI entries.  b = 1 configs weak-scale: the layer has N*m rows,
+each rank owns an m-row shard of every call, and a step is one
+bqg_biqgemm_grouped_sharded_f32 (NCCL broadcast of the G inputs -> grouped
+kernel on the rank's rows -> NCCL all-gather of the G outputs).  The line
+also carries `c5_strong`: BASELINE configs[4] (65536x8192, q2, b8) strong-
+scaled over the N ranks through bqg_biqgemm_sharded_f32, with T(1) measured
+on rank 0's GPU alone in the same run, the efficiency T(1)/(N*T(N)) and a
+bitwise check of y against T(1)'s.  `--config C5` makes that the main line.
 
 --impl reference: the reference's own CPU path (oracle/_ref, the unmodified
 reference headers compiled by oracle/Makefile) on the host cores, same
-config/metric; rank 0 only.
+config/metric; rank 0 only.  That arm loads nothing from this package.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -63,6 +72,7 @@ CONFIGS = {  # name: (m, n, beta, b, mu)
 }
 SEED = 0x5EED
 L2_BYTES = 126 * 1024 * 1024
+GROUP = 128  # calls per grouped launch (one step)
 
 
 def key_bytes(m, n, beta, mu):
@@ -73,20 +83,36 @@ def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config):
-    """Per-launch DRAM bytes of the hot kernel from the committed ncu summary."""
+def ncu_entry(config):
+    """Per-call DRAM traffic of the hot kernel from the committed ncu summary
+    (profiles/ncu_summary.json, one `ncu --set full` capture per config)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
-        d = json.loads(p.read_text())
-        return d.get(config, {}).get("dram_bytes_per_launch")
+        return json.loads(p.read_text()).get(config)
     except Exception:
         return None
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def seq_sum(y):
+    """fp64 sequential sum of y in memory order: the reference shim's checksum."""
+    return float(np.cumsum(np.asarray(y, np.float64).ravel())[-1])
 
 
 class ClockSampler:
@@ -146,277 +172,680 @@ def dist_env():
 # ----------------------------------------------------------------------- ours
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+class Ctx:
+    """Per-process plumbing: device, stream, process group, collectives."""
 
-    rank, local_rank, world = dist_env()
-    # BQG_BENCH_BACKEND=gloo + BQG_BENCH_ONE_DEVICE=1: exercise the multi-rank
-    # control flow on one GPU (test only; the driver's runs use NCCL, one GPU per rank)
-    backend = os.environ.get("BQG_BENCH_BACKEND", "nccl")
-    if os.environ.get("BQG_BENCH_ONE_DEVICE") == "1":
-        local_rank = 0
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        else:
-            dist.init_process_group(backend)
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.rank, local_rank, self.world = dist_env()
+        # BQG_BENCH_BACKEND=gloo + BQG_BENCH_ONE_DEVICE=1: exercise the multi-rank
+        # control flow on one GPU (test only; the driver's runs use NCCL, one GPU per rank)
+        self.backend = os.environ.get("BQG_BENCH_BACKEND", "nccl")
+        if os.environ.get("BQG_BENCH_ONE_DEVICE") == "1":
+            local_rank = 0
+        self.local_rank = local_rank
+        torch.cuda.set_device(local_rank)
+        self.dev = torch.device("cuda", local_rank)
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group(self.backend)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self._coll = None
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def any_rank(self, flag: bool) -> bool:
+        return self.max_over_ranks(1.0 if flag else 0.0) > 0
+
+    def collectives(self):
+        """NCCL through the library (bqg_nccl_*) when the group is NCCL;
+        torch.distributed collectives otherwise (gloo CI runs)."""
+        if self._coll is None:
+            from paper_2005_09904_b200.sharded import NcclComm, TorchCollectives
+
+            if self.world == 1 or self.backend == "nccl":
+                self._coll = NcclComm(self.rank, self.world)
+            else:
+                self._coll = TorchCollectives()
+        return self._coll
+
+    def events(self):
+        return self.torch.cuda.Event(enable_timing=True), self.torch.cuda.Event(enable_timing=True)
+
+    def time_ms(self, fn):
+        """One timed region: barrier + synchronize on both sides, CUDA events
+        on the work stream, max over ranks."""
+        torch = self.torch
+        self.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = self.events()
+        with torch.cuda.stream(self.stream):
+            e0.record(self.stream)
+            fn()
+            e1.record(self.stream)
+        self.stream.synchronize()
+        torch.cuda.synchronize()
+        self.barrier()
+        return self.max_over_ranks(e0.elapsed_time(e1))
+
+
+def steady_replays(ctx, fn, clk, min_s=1.0):
+    """Untimed replays until >= min_s of load (steady clocks under the power
+    cap) and the sampler has readings; all ranks run the same count."""
+    t0 = time.perf_counter()
+    while True:
+        with ctx.torch.cuda.stream(ctx.stream):
+            fn()
+        ctx.stream.synchronize()
+        more = time.perf_counter() - t0 < min_s or (len(clk.samples) < 3 and time.perf_counter() - t0 < 10)
+        if not ctx.any_rank(more):
+            return
+
+
+def timed_replays(ctx, fn, clk):
+    """>= 3 timed regions (and until the sampler has read the clocks during
+    timed work); returns (median ms, all ms, clocks summary)."""
+    n_before = len(clk.samples)
+    times = []
+    while True:
+        times.append(ctx.time_ms(fn))
+        more = len(times) < 3 or (len(clk.samples) <= n_before and len(times) < 200)
+        if not ctx.any_rank(more):
+            break
+    return float(np.median(times)), times, clk.summary(since=n_before)
+
+
+def rotating_copies(ctx, tiled0, alpha0, count_min=2):
+    """Distinct device copies of one layer's tiled keys (+ alpha) totalling
+    > 2x L2, so a call never finds its keys in L2 from an earlier call."""
+    copies = max(count_min, int(np.ceil(2.0 * L2_BYTES / tiled0.numel())) + 1)
+    tiled = [tiled0] + [tiled0.clone() for _ in range(copies - 1)]
+    alphas = [alpha0] + [alpha0.clone() for _ in range(copies - 1)]
+    return tiled, alphas, copies
+
+
+def run_ours(args):
+    ctx = Ctx()
     import paper_2005_09904_b200.biqgemm as bq
 
-    m, n, beta, b, mu = CONFIGS[args.config]
+    cfg = args.config or "C2"
+    m, n, beta, b, mu = CONFIGS[cfg]
     if args.batch:
         b = args.batch  # batch sweep (C4: b = 1 .. 256)
-    kb = key_bytes(m, n, beta, mu)  # per rank and call (weak scaling: each rank owns an m-row shard)
-    dev = torch.device("cuda", local_rank)
-    G = args.group
+    grouped = b == 1 and mu == 8 and beta <= 4
+    if cfg == "C5" and ctx.world > 1:
+        line = c5_main_line(ctx, bq, args)
+    elif grouped:
+        line = run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu)
+    else:
+        line = run_single(ctx, bq, args, cfg, m, n, beta, b, mu)
+    if ctx.world > 1 and cfg != "C5" and not args.no_c5 and not line.get("profile_run"):
+        line["c5_strong"] = c5_strong(ctx, bq, args)
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+    if ctx.world > 1:
+        ctx.barrier()
+        ctx.dist.destroy_process_group()
 
-    # ---- the layer: W generated like bench_cli, quantized + packed on the GPU
-    w = bq.random_uniform(m * world, n, SEED) if world > 1 else bq.random_uniform(m, n, SEED)
-    w_shard = np.ascontiguousarray(w[rank * m:(rank + 1) * m])
-    layer = bq.PackedLinear.from_weights(w_shard, beta, mu)
-    keys, alpha = layer.export()
 
-    # ---- rotating weight copies > 2x L2 (every call streams its keys from
-    # HBM), one x per copy (every call builds its own LUT)
-    tiled0 = bq.tile_keys(torch.from_numpy(keys).to(dev), n, mu)
-    copies = max(2, int(np.ceil(2.0 * L2_BYTES / tiled0.numel())) + 1)
-    tiled = [tiled0] + [tiled0.clone() for _ in range(copies - 1)]
-    alphas = [torch.from_numpy(alpha).to(dev) for _ in range(copies)]
-    x_h = [bq.random_normal(n, b, SEED + 1 + j) for j in range(copies)]
-    xs = [torch.from_numpy(x).to(dev) for x in x_h]
-    ys = [torch.empty((m, b), device=dev) for _ in range(copies)]
-    stream = torch.cuda.Stream(device=dev)
+def make_layer(ctx, bq, m, n, beta, mu, rows=None):
+    """The bench_cli layer (W = random_uniform(rows x n, 0x5EED)), this rank's
+    m-row shard quantized + packed on the GPU."""
+    M = rows or m
+    w = bq.random_uniform(M, n, SEED)
+    lo = ctx.rank * m if rows else 0
+    return bq.PackedLinear.from_weights(np.ascontiguousarray(w[lo:lo + m]), beta, mu)
 
-    # ---- correctness gate before timing: y equals the exact path within tolerance
-    ws_g = bq.grouped_workspace(m, n, b, beta, mu, G, device=dev)
-    with torch.cuda.stream(stream):
-        bq.biqgemm_grouped_device([(tiled[j], alphas[j], xs[j], ys[j]) for j in range(2)], n, m, n, b, beta, mu,
-                                  ws_g, stream=stream.cuda_stream)
-    stream.synchronize()
+
+def parity_gate(bq, layer, ys_dev, x_h, count=2):
+    """y of the first calls equals the exact path (bit-identical to the
+    reference) within the fp32 contract before anything is timed."""
     rel = 0.0
-    for j in range(2):
+    for j in range(count):
         y_exact = layer.forward(x_h[j], exact=True)
-        y0 = ys[j].cpu().numpy()
+        y0 = ys_dev[j].cpu().numpy().reshape(y_exact.shape)
         rel = max(rel, float(np.linalg.norm(y0.astype(np.float64) - y_exact) /
                              np.linalg.norm(y_exact.astype(np.float64))))
     assert rel <= 1e-5, f"parity gate failed: rel {rel}"
+    return rel
 
-    # ---- throughput graph: `count` independent calls, G per grouped launch
-    def grouped_graph(count, offset):
-        arrays = []
-        for st in range(offset, offset + count, G):
-            ent = [(tiled[i % copies], alphas[i % copies], xs[i % copies], ys[i % copies])
-                   for i in range(st, min(offset + count, st + G))]
-            arrays.append(bq.make_calls(ent))
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(g, stream=stream):
-                for a in arrays:
-                    bq.biqgemm_grouped_device(a, n, m, n, b, beta, mu, ws_g, pdl=True, stream=stream.cuda_stream)
-        return g, len(arrays)
 
-    # ---- latency graph: dependent-layer regime, one kernel (chain) per call
-    ws1 = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, b, beta, mu)), device=dev)
+def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
+    torch = ctx.torch
+    dev, stream, world, rank = ctx.dev, ctx.stream, ctx.world, ctx.rank
+    G, K, W = args.group, args.steps, args.warmup
+    kb = key_bytes(m, n, beta, mu)  # per rank and call (weak scaling: each rank owns an m-row shard)
 
-    def chain_graph(count):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            bq.biqgemm_device(tiled[0], alphas[0], xs[0], ys[0], m, n, beta, mu, ws1, pdl=True,
-                              stream=stream.cuda_stream)
-            stream.synchronize()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(count):
-                    j = i % copies
-                    bq.biqgemm_device(tiled[j], alphas[j], xs[j], ys[j], m, n, beta, mu, ws1, pdl=True,
-                                      stream=stream.cuda_stream)
-        return g
+    layer = make_layer(ctx, bq, m, n, beta, mu, rows=world * m if world > 1 else None)
+    keys, alpha = layer.export()
+    tiled, alphas, copies = rotating_copies(ctx, bq.tile_keys(torch.from_numpy(keys).to(dev), n, mu),
+                                            torch.from_numpy(alpha).to(dev))
+    NX = 8  # distinct inputs per step slot
+    x_h = [bq.random_normal(n, b, SEED + 1 + j) for j in range(NX)]
+    x_step = torch.from_numpy(np.stack([x_h[i % NX] for i in range(G)])).to(dev)  # [G, n, 1]
+    R = m  # rows per rank (m is 32-aligned)
+    y_gather = torch.empty((world, G, R, b), device=dev)
+    y_mine = y_gather[rank]
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_workspace_bytes(world * m, n, b, beta, mu, G, world))
+                      if world > 1 else int(bq.lib.bqg_biqgemm_grouped_workspace_bytes(m, n, b, beta, mu, G)),
+                      device=dev)
 
-    g_warm, _ = grouped_graph(max(args.warmup, 1), 0)
-    g_timed, n_launch = grouped_graph(args.steps, args.warmup)
-    torch.cuda.synchronize()
+    def step_calls(s):
+        """Calls of step s: call i uses weight copy (s*G + i) mod R."""
+        return [(tiled[(s * G + i) % copies], alphas[(s * G + i) % copies]) for i in range(G)]
 
-    def timed(g):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            g.replay()
-            e1.record(stream)
-        stream.synchronize()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        return e0.elapsed_time(e1)
-
-    if args.profile:
-        # under ncu: W warm-up calls, one timed replay, and a short single-call chain
-        with torch.cuda.stream(stream):
-            g_warm.replay()
-            g_timed.replay()
-        g_chain = chain_graph(16)
-        with torch.cuda.stream(stream):
-            g_chain.replay()
-        torch.cuda.synchronize()
-        if rank == 0:
-            print(json.dumps({"profile_run": True, "config": args.config, "steps": args.steps, "group": G}))
-        return
-    with ClockSampler(local_rank) as clk:
-        # warm-up steps + enough untimed replays for steady clocks (>= 1 s,
-        # and until the sampler has readings under load)
-        with torch.cuda.stream(stream):
-            g_warm.replay()
-            t0 = time.perf_counter()
-            while True:
-                g_timed.replay()
-                stream.synchronize()
-                more = time.perf_counter() - t0 < 1.0 or (len(clk.samples) < 3 and time.perf_counter() - t0 < 10)
-                if world > 1:
-                    flag = torch.tensor([1.0 if more else 0.0], device=dev)
-                    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-                    more = bool(flag.item() > 0)
-                if not more:
-                    break
-        n_before = len(clk.samples)
-        ms = 0.0
-        reps = 0
-        # the timed region: one replay of exactly K steps, bracketed by
-        # barrier + synchronize; repeated (>= 3 times, and until the sampler
-        # has read the clocks during timed work); the MEDIAN replay is reported
-        times = []
-        while True:
-            times.append(timed(g_timed))
-            reps += 1
-            more = reps < 3 or (len(clk.samples) <= n_before and reps < 200)
-            if world > 1:  # every rank runs the same number of (barrier-bracketed) replays
-                flag = torch.tensor([1.0 if more else 0.0], device=dev)
-                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-                more = bool(flag.item() > 0)
-            if not more:
-                break
-        ms = float(np.median(times))
-        clocks = clk.summary(since=n_before)
-
-    # y of every call is assembled across ranks (N>1): one NCCL all-gather
-    # per grouped launch (G calls' row shards), timed as part of the step
-    gather_ms = 0.0
+    # host call arrays, built once per step (the launches below only pass them)
+    local_arrays = [bq.make_calls([(t, a, x_step[i], y_mine[i]) for i, (t, a) in enumerate(step_calls(s))])
+                    for s in range(W + K)]
+    shard_arrays = []
     if world > 1:
-        y_grp = torch.empty((G, m, b), device=dev)
-        y_all = torch.empty((world * G, m, b), device=dev)
-        for _ in range(3):
-            dist.all_gather_into_tensor(y_all, y_grp)
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(n_launch):
-            dist.all_gather_into_tensor(y_all, y_grp)
-        e1.record()
-        torch.cuda.synchronize()
-        gather_ms = e0.elapsed_time(e1)
-        t = torch.tensor([ms + gather_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    else:
-        total_ms = ms
+        for s in range(W + K):
+            arr = (bq._capi.ShardCall * G)()
+            for i, (t, a) in enumerate(step_calls(s)):
+                arr[i] = bq._capi.ShardCall(t.data_ptr(), a.data_ptr())
+            shard_arrays.append(arr)
 
-    per_call_s = ms * 1e-3 / args.steps
-    kernel_gbs = kb / per_call_s / 1e9
-    value_gbs = world * kb * args.steps / (total_ms * 1e-3) / 1e9
-    peak, peak_kind = measured_peaks()
+    def local_launch(s, pdl=True):
+        """The grouped kernel alone on this rank's rows (compute only)."""
+        bq.biqgemm_grouped_device(local_arrays[s], n, m, n, b, beta, mu, ws, pdl=pdl, stream=stream.cuda_stream)
 
-    # dependent-call latency (each call waits for its predecessor)
-    lat_steps = min(args.steps, 2000)
-    g_chain = chain_graph(lat_steps)
+    coll = ctx.collectives() if world > 1 else None
+    if hasattr(coll, "register"):
+        coll.register(x_step, y_gather)
+    coll_struct = coll.collectives() if coll is not None else None
+
+    def sharded_launch(s, pdl=True):
+        """One step at N > 1: broadcast x -> grouped kernel -> all-gather y (C ABI)."""
+        import ctypes as C
+
+        bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
+            C.cast(shard_arrays[s], C.c_void_p), G, x_step.data_ptr(), n, y_gather.data_ptr(), world * m, n, b, beta,
+            mu, rank, world, C.byref(coll_struct), ws.ptr(), ws.nbytes, 1 if pdl else 0, stream.cuda_stream))
+
+    # ---- correctness gate before timing
     with torch.cuda.stream(stream):
-        g_chain.replay()
-    lat_ms = timed(g_chain)
-    lat_us = lat_ms * 1e3 / lat_steps
-    del g_chain
+        (sharded_launch if world > 1 else local_launch)(0, pdl=False)
+    stream.synchronize()
+    rel = parity_gate(bq, layer, [y_mine[i] for i in range(2)], [x_h[i % NX] for i in range(2)])
 
-    # ---- e2e through the public C ABI with HOST buffers (pinned): per group
-    # of G calls one bqg_layers_forward_host = H2D of the G inputs, the
-    # grouped kernels, D2H of the G outputs, synchronised
-    e2e_layers = [layer] + [bq.PackedLinear.from_keys(keys, alpha, n, mu) for _ in range(copies - 1)]
-    GE = args.e2e_group  # calls per synchronised API call (the library pipelines copies inside it)
-    x_pin = torch.from_numpy(np.stack([x_h[i % copies] for i in range(GE)])).pin_memory()
-    y_pin = torch.empty((GE, m, b), dtype=torch.float32).pin_memory()
-    groups = [bq.LayerGroup([e2e_layers[(st + i) % copies] for i in range(min(GE, args.steps - st))])
-              for st in range(0, args.steps, GE)]
-    for grp in groups[:2]:
-        bq.layers_forward_into(grp, x_pin[:len(grp)], y_pin[:len(grp)])
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for grp in groups:
-        bq.layers_forward_into(grp, x_pin[:len(grp)], y_pin[:len(grp)])
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    y_check = layer.forward(np.ascontiguousarray(x_pin[0].numpy()), exact=True)
-    assert np.allclose(y_pin[0].numpy(), y_check, rtol=0, atol=1e-5 * np.abs(y_check).max())
-    e2e_gbs = world * kb * args.steps / e2e_s / 1e9
+    # ---- the timed step sequence: K grouped launches
+    use_graph = world == 1
+    if use_graph:
+        def capture(first, count):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(stream):
+                with torch.cuda.graph(g, stream=stream):
+                    for s in range(first, first + count):
+                        local_launch(s)
+            return g
 
-    stream_form = b == 1 and mu == 8 and beta <= 4
+        g_warm, g_timed = capture(0, W), capture(W, K)
+        run_warm, run_timed = g_warm.replay, g_timed.replay
+    else:
+        def run_warm():
+            for s in range(W):
+                sharded_launch(s)
+
+        def run_timed():
+            for s in range(W, W + K):
+                sharded_launch(s)
+
+    peak, peak_kind = measured_peaks()
+    if args.profile:
+        # under ncu: the warm-up steps, one timed sequence and a short dependent chain
+        with torch.cuda.stream(stream):
+            run_warm()
+            run_timed()
+        latency_chain(ctx, bq, tiled, alphas, x_step, y_mine, m, n, beta, mu, b, kb, peak, 16, timed=False)
+        torch.cuda.synchronize()
+        return {"profile_run": True, "config": cfg, "steps": K, "group": G}
+    with ClockSampler(ctx.local_rank) as clk:
+        with torch.cuda.stream(stream):
+            run_warm()
+        steady_replays(ctx, run_timed, clk)
+        ms, all_ms, clocks = timed_replays(ctx, run_timed, clk)
+        compute_ms = None
+        if world > 1:  # the same launches without the collectives
+            def run_compute():
+                for s in range(W, W + K):
+                    local_launch(s)
+            compute_ms, _, _ = timed_replays(ctx, run_compute, clk)
+    calls = K * G
+    per_call_s = ms * 1e-3 / calls
+    value_gbs = world * kb * calls / (ms * 1e-3) / 1e9
+    kernel_ms_per_launch = (compute_ms if compute_ms is not None else ms) / K
+    achieved = kb * G / (kernel_ms_per_launch * 1e-3) / 1e9
+
     line = {
         "metric": METRIC,
         "value": round(value_gbs, 2),
         "unit": "GB/s",
         "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": ms / K,
         "us_per_call": per_call_s * 1e6,
-        "hbm_frac_of_peak": kernel_gbs / peak,
+        "hbm_frac_of_peak": round(achieved / peak, 4),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u8 keys, f32 LUT/accumulate",
-        "data": "synthetic (bench_cli generator: W=random_uniform(m,n,0x5EED), x=random_normal(n,b,0x5EED+1+j))",
-        "config": {"workload": f"{args.config} m={m} n={n} q={beta} mu={mu} b={b}" + (
-            f" per rank (layer {world * m}x{n}, y all-gathered with NCCL)" if world > 1 else ""),
+        "dtype": "u8 keys, f32 LUT/accumulate, f64 alpha epilogue",
+        "data": "synthetic (bench_cli generator: W=random_uniform(m,n,0x5EED), x=random_normal(n,b,0x5EED+1+j)); "
+                "quantized + packed on the GPU",
+        "config": {"workload": f"{cfg} m={m} n={n} q={beta} mu={mu} b={b}" + (
+            f" per rank (layer {world * m}x{n} row-sharded over {world} GPUs)" if world > 1 else ""),
                    "m": m, "n": n, "beta": beta, "mu": mu, "batch": b,
-                   "step": "one BiQGEMM call (own weights copy, own x, own LUT build, y written)",
-                   "l2": f"inputs larger than L2: {copies} rotating weight copies = "
-                         f"{copies * tiled0.numel() / 1e6:.0f} MB > 2x126 MB",
-                   "timing": f"CUDA graph of {n_launch} grouped launches ({G} independent calls each, "
-                             f"{'stream form' if stream_form else 'single-call kernels'}), CUDA events",
+                   "step": f"one grouped launch of {G} independent BiQGEMM calls (own weight copy, own x, own LUT "
+                           f"build, own y each)" + ("; NCCL broadcast of the x batch + all-gather of the y batch "
+                                                    "inside the step (bqg_biqgemm_grouped_sharded_f32)"
+                                                    if world > 1 else ""),
+                   "l2": f"inputs larger than L2: every call reads a different one of {copies} rotating weight "
+                         f"copies ({copies * tiled[0].numel() / 1e6:.0f} MB > 2x126 MB L2) at any --steps",
+                   "timing": f"{'CUDA graph of ' if use_graph else ''}{K} grouped launches ({calls} calls) per timed "
+                             f"region, CUDA events on the launch stream, median of {len(all_ms)} regions after >= 1 s "
+                             f"of untimed replays (steady clocks)",
                    "parallelism": f"rows x{world}"},
-        "roofline": {"bound": "hbm", "achieved": round(kernel_gbs, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(kernel_gbs / peak, 4), "traffic": ncu_traffic(args.config),
-                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": kb * min(G, args.steps),
-                     "kernel": "biqgemm_stream_kernel + stream_finalize_kernel" if stream_form else "fast path"},
-        "latency": {"us_per_call": round(lat_us, 3), "gbs": round(kb / (lat_us * 1e-6) / 1e9, 1),
-                    "frac": round(kb / (lat_us * 1e-6) / 1e9 / peak, 4),
-                    "form": "dependent-call regime: one single-call kernel per step, PDL-chained CUDA graph"},
-        "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": int(x_h[0].nbytes),
-                "d2h_bytes_per_step": int(m * b * 4), "us_per_call": e2e_s / args.steps * 1e6,
-                "api": f"bqg_layers_forward_host, {GE} calls per synchronised API call "
-                       "(H2D / grouped kernels / D2H pipelined inside the call in sub-groups ramping "
-                       "sized by host I/O, C2: 64-128-256..128-64 calls; LayerGroup handle array built once)"},
-        "gpu_launches": 2 * n_launch if stream_form else args.steps * 2,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": kb * G,
+                     "algorithmic_bytes_per_call": kb,
+                     "launch_ms": kernel_ms_per_launch,
+                     "kernel": "biqgemm_tex_kernel (grouped form: LUT build, gather, alpha epilogue and the "
+                               "final block sum in one kernel)"},
+        "gpu_launches": K,
         "clocks": clocks,
         "parity_rel_fro": rel,
     }
+    ncu = ncu_entry(cfg)
+    if ncu and world == 1:
+        per_call = ncu["dram_bytes_per_launch"] / ncu["calls_per_launch"]
+        line["roofline"]["traffic"] = round(per_call * G)
+        line["roofline"]["traffic_per_call"] = round(per_call)
+        line["roofline"]["traffic_over_algorithmic"] = round(per_call / kb, 4)
+        line["roofline"]["traffic_source"] = ncu.get("source")
+    else:
+        line["roofline"]["traffic"] = None
     if world > 1:
-        line["allgather_ms_total"] = gather_ms
+        line["compute_ms_per_step"] = compute_ms / K
+        line["collective_ms_per_step"] = (ms - compute_ms) / K
+
+    if world == 1:
+        line["latency"] = latency_chain(ctx, bq, tiled, alphas, x_step, y_mine, m, n, beta, mu, b, kb, peak,
+                                        args.latency_calls)
+        if not args.no_sweep:
+            line["group_sweep"] = group_sweep(ctx, bq, tiled, alphas, x_step, y_mine, m, n, beta, mu, b, kb, peak)
+    line["e2e"] = e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K)
     if world == 1 and not args.no_comparators:
-        line["comparators"] = comparators(bq, layer, w_shard, x_h, m, n, beta, b, mu, kb, dev)
+        line["comparators"] = comparators(bq, layer, x_h, m, n, beta, b, mu, kb, ctx.dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, keys, alpha, x_h[0], m, n, beta, mu, b, args.cpu_seconds)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    for L in e2e_layers:
-        L.close()
-    if world > 1:
-        dist.destroy_process_group()
+        line["cpu_baseline"] = cpu_baseline(cfg, keys, alpha, x_h[0], m, n, beta, mu, b, args.cpu_seconds)
+        line["parity_vs_reference"] = reference_checksum_parity(bq, layer, x_h[0], line["cpu_baseline"])
+    if world == 1 and not args.no_c5:
+        line["c5_strong"] = c5_strong(ctx, bq, args)
+    layer.close()
+    return line
 
 
-def comparators(bq, layer, w, x_h, m, n, beta, b, mu, kb, dev, calls=200):
+def latency_chain(ctx, bq, tiled, alphas, x_step, y_mine, m, n, beta, mu, b, kb, peak, count, timed=True):
+    """Dependent-call regime: `count` single-call kernels, each PDL-chained
+    behind its predecessor (consecutive layers of one model)."""
+    torch, stream = ctx.torch, ctx.stream
+    copies = len(tiled)
+    ws1 = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, b, beta, mu)), device=ctx.dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        bq.biqgemm_device(tiled[0], alphas[0], x_step[0], y_mine[0], m, n, beta, mu, ws1, pdl=True,
+                          stream=stream.cuda_stream)
+        stream.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(count):
+                bq.biqgemm_device(tiled[i % copies], alphas[i % copies], x_step[i % x_step.shape[0]],
+                                  y_mine[i % y_mine.shape[0]], m, n, beta, mu, ws1, pdl=True,
+                                  stream=stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+    if not timed:
+        return None
+    ms = float(np.median([ctx.time_ms(g.replay) for _ in range(3)]))
+    us = ms * 1e3 / count
+    form = int(bq.lib.bqg_biqgemm_form(m, n, b, beta, mu))
+    return {"us_per_call": round(us, 3), "gbs": round(kb / (us * 1e-6) / 1e9, 1),
+            "frac": round(kb / (us * 1e-6) / 1e9 / peak, 4), "calls": count,
+            "form": f"dependent-call regime: {count} single-call kernels (form {form}), each PDL-chained behind its "
+                    "predecessor in a CUDA graph; median of 3"}
+
+
+def group_sweep(ctx, bq, tiled, alphas, x_step, y_mine, m, n, beta, mu, b, kb, peak):
+    """us/call vs calls per grouped launch (rotating copies > 2x L2, >= 1024 calls per region)."""
+    torch, stream = ctx.torch, ctx.stream
+    copies = len(tiled)
+    out = {}
+    for Gs in (1, 3, 8, 32, 128, 512):
+        ws = bq.grouped_workspace(m, n, b, beta, mu, Gs, device=ctx.dev)
+        launches = max(4, 1024 // Gs)
+        xs = [x_step[i % x_step.shape[0]] for i in range(Gs)]
+        ys = [torch.empty((m, b), device=ctx.dev) for _ in range(min(Gs, 512))]
+        arrays = [bq.make_calls([(tiled[(L * Gs + i) % copies], alphas[(L * Gs + i) % copies], xs[i], ys[i])
+                                 for i in range(Gs)]) for L in range(launches)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            bq.biqgemm_grouped_device(arrays[0], n, m, n, b, beta, mu, ws, pdl=False, stream=stream.cuda_stream)
+            stream.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                for a in arrays:
+                    bq.biqgemm_grouped_device(a, n, m, n, b, beta, mu, ws, pdl=True, stream=stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        ms = float(np.median([ctx.time_ms(g.replay) for _ in range(3)]))
+        us = ms * 1e3 / (launches * Gs)
+        out[str(Gs)] = {"us_per_call": round(us, 3), "frac": round(kb / (us * 1e-6) / 1e9 / peak, 4)}
+        del g
+    return out
+
+
+def e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K):
+    """The same step through the public API with HOST buffers, wall clock,
+    max over ranks.  N=1: bqg_layers_forward_host (one synchronised API call
+    per step of G calls).  N>1: rank 0's pinned x batch -> H2D ->
+    bqg_biqgemm_grouped_sharded_f32 -> D2H of the gathered y batch."""
+    torch = ctx.torch
+    world = ctx.world
+    x_pin = torch.from_numpy(np.stack([x_h[i % len(x_h)] for i in range(G)])).pin_memory()
+    if world == 1:
+        n_layers = max(2, int(np.ceil(2.0 * L2_BYTES / bq.tiled_key_bytes(m, n, beta, mu))) + 1)
+        layers = [layer] + [bq.PackedLinear.from_keys(keys, alpha, n, mu) for _ in range(n_layers - 1)]
+        y_pin = torch.empty((G, m, b), dtype=torch.float32).pin_memory()
+        groups = [bq.LayerGroup([layers[(s * G + i) % n_layers] for i in range(G)]) for s in range(min(K, 8))]
+        for grp in groups[:2]:
+            bq.layers_forward_into(grp, x_pin, y_pin)
+        t0 = time.perf_counter()
+        for s in range(K):
+            bq.layers_forward_into(groups[s % len(groups)], x_pin, y_pin)
+        e2e_s = time.perf_counter() - t0
+        y_check = layer.forward(np.ascontiguousarray(x_pin[0].numpy()), exact=True)
+        assert np.allclose(y_pin[0].numpy(), y_check, rtol=0, atol=1e-5 * np.abs(y_check).max())
+        for L in layers[1:]:
+            L.close()
+        api = (f"bqg_layers_forward_host: one synchronised API call per step ({G} calls; H2D / grouped kernels / "
+               "D2H pipelined inside the call in sub-groups sized by host I/O)")
+        d2h = G * m * b * 4
+    else:
+        import ctypes as C
+
+        dev, stream = ctx.dev, ctx.stream
+        tiled0 = bq.tile_keys(torch.from_numpy(keys).to(dev), n, mu)
+        al0 = torch.from_numpy(alpha).to(dev)
+        n_copies = max(2, int(np.ceil(2.0 * L2_BYTES / tiled0.numel())) + 1)
+        tl = [tiled0] + [tiled0.clone() for _ in range(n_copies - 1)]
+        x_dev = torch.empty((G, n, b), device=dev)
+        y_gather = torch.empty((world, G, m, b), device=dev)
+        y_host = torch.empty((world, G, m, b), dtype=torch.float32).pin_memory()
+        ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_workspace_bytes(world * m, n, b, beta, mu, G, world)),
+                          device=dev)
+        coll = ctx.collectives()
+
+        arrays = []
+        for s in range(8):
+            arr = (bq._capi.ShardCall * G)()
+            for i in range(G):
+                arr[i] = bq._capi.ShardCall(tl[(s * G + i) % n_copies].data_ptr(), al0.data_ptr())
+            arrays.append(arr)
+        if hasattr(coll, "register"):
+            coll.register(x_dev, y_gather)
+        cs = coll.collectives()
+
+        def one(s):
+            if ctx.rank == 0:
+                x_dev.copy_(x_pin, non_blocking=True)
+            bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
+                C.cast(arrays[s % 8], C.c_void_p), G, x_dev.data_ptr(), n, y_gather.data_ptr(), world * m, n, b,
+                beta, mu, ctx.rank, world, C.byref(cs), ws.ptr(), ws.nbytes, 0, stream.cuda_stream))
+            if ctx.rank == 0:
+                y_host.copy_(y_gather, non_blocking=True)
+            stream.synchronize()
+
+        with torch.cuda.stream(stream):
+            one(0)
+            ctx.barrier()
+            t0 = time.perf_counter()
+            for s in range(K):
+                one(s)
+            e2e_s = time.perf_counter() - t0
+        api = ("bqg_biqgemm_grouped_sharded_f32 per step: rank 0 H2D of the pinned x batch, NCCL broadcast, grouped "
+               "kernel on each rank's rows, NCCL all-gather, rank 0 D2H of the gathered y batch, synchronised")
+        d2h = world * G * m * b * 4
+    e2e_s = ctx.max_over_ranks(e2e_s)
+    return {"value": round(world * kb * G * K / e2e_s / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(G * x_h[0].nbytes), "d2h_bytes_per_step": int(d2h),
+            "us_per_call": e2e_s / (K * G) * 1e6, "api": api}
+
+
+def run_single(ctx, bq, args, cfg, m, n, beta, b, mu):
+    """b > 1 (or non-grouped) configs at N=1: a step is one call on its own
+    weight copy, K calls PDL-chained in a CUDA graph."""
+    torch, dev, stream = ctx.torch, ctx.dev, ctx.stream
+    K, W = args.steps, args.warmup
+    kb = key_bytes(m, n, beta, mu)
+    layer = make_layer(ctx, bq, m, n, beta, mu)
+    keys, alpha = layer.export()
+    tiled, alphas, copies = rotating_copies(ctx, bq.tile_keys(torch.from_numpy(keys).to(dev), n, mu),
+                                            torch.from_numpy(alpha).to(dev))
+    x_h = [bq.random_normal(n, b, SEED + 1 + j) for j in range(4)]
+    xs = [torch.from_numpy(x).to(dev) for x in x_h]
+    ys = [torch.empty((m, b), device=dev) for _ in range(4)]
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, b, beta, mu)), device=dev)
+
+    def launch(i):
+        bq.biqgemm_device(tiled[i % copies], alphas[i % copies], xs[i % 4], ys[i % 4], m, n, beta, mu, ws, pdl=True,
+                          stream=stream.cuda_stream)
+
+    with torch.cuda.stream(stream):
+        launch(0)
+        launch(1)
+    stream.synchronize()
+    rel = parity_gate(bq, layer, ys[:2], x_h[:2])
+
+    def capture(first, count):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(first, first + count):
+                    launch(i)
+        return g
+
+    g_warm, g_timed = capture(0, W), capture(W, K)
+    peak, peak_kind = measured_peaks()
+    with ClockSampler(ctx.local_rank) as clk:
+        with torch.cuda.stream(stream):
+            g_warm.replay()
+        steady_replays(ctx, g_timed.replay, clk, min_s=0.5)
+        ms, all_ms, clocks = timed_replays(ctx, g_timed.replay, clk)
+    us = ms * 1e3 / K
+    gbs = kb / (us * 1e-6) / 1e9
+    lds_us = 4.0 * beta * m * ((n + mu - 1) // mu) * b / (128.0 * 148 * 1.92e9) * 1e6
+    line = {
+        "metric": METRIC, "value": round(gbs, 2), "unit": "GB/s", "n_gpus": 1, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "us_per_call": us, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8 keys, f32 LUT/accumulate, f64 alpha epilogue",
+        "data": "synthetic (bench_cli generator); quantized + packed on the GPU",
+        "config": {"workload": f"{cfg} m={m} n={n} q={beta} mu={mu} b={b}", "m": m, "n": n, "beta": beta, "mu": mu,
+                   "batch": b, "step": "one BiQGEMM call on its own weight copy",
+                   "l2": f"{copies} rotating weight copies ({copies * tiled[0].numel() / 1e6:.0f} MB > 2x126 MB L2)",
+                   "timing": f"CUDA graph of {K} PDL-chained calls, CUDA events, median of {len(all_ms)}",
+                   "parallelism": "rows x1", "form": int(bq.lib.bqg_biqgemm_form(m, n, b, beta, mu))},
+        "roofline": {"bound": "lds" if b > 1 else "hbm",
+                     "achieved": round(gbs, 1), "unit": "GB/s", "peak": peak, "peak_kind": peak_kind,
+                     "frac": round(gbs / peak, 4),
+                     "lds_gather_floor_us": round(lds_us, 2), "lds_frac": round(lds_us / us, 4),
+                     "algorithmic_bytes_per_call": kb, "traffic": None},
+        "gpu_launches": 2 * K, "clocks": clocks, "parity_rel_fro": rel,
+    }
+    # e2e: the public host-buffer entry (bqg_layer_forward_host: H2D of x, the
+    # kernels, D2H of y, synchronised), one call per step, wall clock
+    x_pin = torch.from_numpy(x_h[0]).pin_memory()
+    y_pin = torch.empty((m, b), dtype=torch.float32).pin_memory()
+    for _ in range(3):
+        layer.forward_into(x_pin, y_pin)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        layer.forward_into(x_pin, y_pin)
+    e2e_s = (time.perf_counter() - t0) / K
+    line["e2e"] = {"value": round(kb / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(x_h[0].nbytes),
+                   "d2h_bytes_per_step": int(m * b * 4), "us_per_call": e2e_s * 1e6,
+                   "api": "bqg_layer_forward_host per step (one layer: its keys stay L2-resident across steps)"}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, keys, alpha, x_h[0], m, n, beta, mu, b, args.cpu_seconds)
+        line["parity_vs_reference"] = reference_checksum_parity(bq, layer, x_h[0], line["cpu_baseline"])
+    layer.close()
+    return line
+
+
+# ---------------------------------------------------- C5 strong scaling
+
+
+def c5_inputs(bq):
+    """C5 (BASELINE configs[4]): 65536x8192, q2, mu 8, b 8.  Keys and alpha are
+    seeded random (identical on every rank), x from the bench_cli generator."""
+    m, n, beta, b, mu = CONFIGS["C5"]
+    rng = np.random.default_rng(SEED)
+    G = (n + mu - 1) // mu
+    keys = rng.integers(0, 256, size=(beta, m, G), dtype=np.uint8)
+    alpha = rng.uniform(0.01, 0.1, size=(beta, m)).astype(np.float32)
+    x = bq.random_normal(n, b, SEED + 1)
+    return keys, alpha, x
+
+
+def c5_time(ctx, bq, keys, alpha, x, rank, world, coll, K, W):
+    """T(world) of C5 through bqg_biqgemm_sharded_f32 on ranks 0..world-1 of
+    `coll` (this process's share), rotating shard copies > 2x L2.  Returns
+    (ms per call end to end, ms per call compute only, y checksum bytes)."""
+    import ctypes as C
+
+    torch, dev, stream = ctx.torch, ctx.dev, ctx.stream
+    m, n, beta, b, mu = CONFIGS["C5"]
+    lo, hi, R = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    bq.check(bq.lib.bqg_shard_rows(m, world, rank, C.byref(lo), C.byref(hi), C.byref(R)))
+    lo, hi, R = lo.value, hi.value, R.value
+    t0 = bq.tile_keys(torch.from_numpy(np.ascontiguousarray(keys[:, lo:hi])).to(dev), n, mu)
+    a0 = torch.from_numpy(np.ascontiguousarray(alpha[:, lo:hi])).to(dev)
+    tiled, alphas, copies = rotating_copies(ctx, t0, a0)
+    x_dev = torch.from_numpy(x).to(dev)
+    y_gather = torch.empty((world * R, b), device=dev)
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_workspace_bytes(m, n, b, beta, mu, world)), device=dev)
+    if hasattr(coll, "register"):
+        coll.register(x_dev, y_gather)
+    cs = coll.collectives()
+
+    def call(i):
+        bq.check(bq.lib.bqg_biqgemm_sharded_f32(tiled[i % copies].data_ptr(), alphas[i % copies].data_ptr(),
+                                                x_dev.data_ptr(), n, y_gather.data_ptr(), m, n, b, beta, mu, rank,
+                                                world, C.byref(cs), ws.ptr(), ws.nbytes, stream.cuda_stream))
+
+    def compute(i):
+        bq.biqgemm_device(tiled[i % copies], alphas[i % copies], x_dev, y_gather[rank * R: rank * R + (hi - lo)],
+                          hi - lo, n, beta, mu, ws, pdl=True, stream=stream.cuda_stream)
+
+    with torch.cuda.stream(stream):
+        for i in range(W):
+            call(i)
+    stream.synchronize()
+    y = y_gather[:m].cpu().numpy()
+    digest = hashlib.sha256(y.tobytes()).hexdigest()
+    sub = ctx if world == ctx.world else _Solo(ctx)
+    e2e = float(np.median([sub.time_ms(lambda: [call(i) for i in range(K)]) for _ in range(3)])) / K
+    comp = float(np.median([sub.time_ms(lambda: [compute(i) for i in range(K)]) for _ in range(3)])) / K
+    return e2e, comp, digest
+
+
+class _Solo:
+    """time_ms on this rank alone (T(1) inside a multi-rank run)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+
+    def time_ms(self, fn):
+        torch, stream = self.ctx.torch, self.ctx.stream
+        torch.cuda.synchronize()
+        e0, e1 = self.ctx.events()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        stream.synchronize()
+        return e0.elapsed_time(e1)
+
+
+def c5_strong(ctx, bq, args):
+    """BASELINE configs[4] strong-scaled over this run's ranks (north_star:
+    row shards, x broadcast, y all-gathered with NCCL); T(1) on rank 0 alone."""
+    from paper_2005_09904_b200.sharded import NcclComm
+
+    m, n, beta, b, mu = CONFIGS["C5"]
+    K, W = args.c5_steps, 3
+    keys, alpha, x = c5_inputs(bq)
+    kb = key_bytes(m, n, beta, mu)
+    out = {"workload": f"C5 m={m} n={n} q={beta} mu={mu} b={b}", "steps": K,
+           "step": "one row-sharded call: NCCL broadcast of x -> fused kernel on the rank's rows -> NCCL all-gather "
+                   "of y (bqg_biqgemm_sharded_f32)",
+           "data": "seeded random keys/alpha (identical on every rank), x = random_normal(n,b,0x5EED+1)"}
+    t1 = comp1 = None
+    digest1 = None
+    if ctx.rank == 0:
+        solo = NcclComm(0, 1) if (ctx.world == 1 or ctx.backend == "nccl") else None
+        if solo is not None:
+            t1, comp1, digest1 = c5_time(ctx, bq, keys, alpha, x, 0, 1, solo, K, W)
+            solo.close()
+    ctx.barrier()
+    if ctx.world == 1:
+        out.update({"t1_ms": t1, "t1_compute_ms": comp1, "t1_gbs": round(kb / (t1 * 1e-3) / 1e9, 1),
+                    "y_sha256": digest1})
+        return out
+    tN, compN, digestN = c5_time(ctx, bq, keys, alpha, x, ctx.rank, ctx.world, ctx.collectives(), K, W)
+    out.update({"n": ctx.world, "tN_ms": tN, "tN_compute_ms": compN, "t1_ms": t1, "t1_compute_ms": comp1,
+                "tN_gbs": round(kb / (tN * 1e-3) / 1e9, 1)})
+    if t1:
+        out["efficiency"] = round(t1 / (ctx.world * tN), 4)
+        out["compute_efficiency"] = round(comp1 / (ctx.world * compN), 4)
+        out["y_bitwise_equal_to_t1"] = digestN == digest1
+    return out
+
+
+def c5_main_line(ctx, bq, args):
+    """--config C5 at N > 1: the strong-scaling run is the line."""
+    s = c5_strong(ctx, bq, args)
+    m, n, beta, b, mu = CONFIGS["C5"]
+    kb = key_bytes(m, n, beta, mu)
+    peak, peak_kind = measured_peaks()
+    return {"metric": METRIC, "value": s["tN_gbs"], "unit": "GB/s", "n_gpus": ctx.world, "steps": s["steps"],
+            "warmup": 3, "ms_per_step": s["tN_ms"], "us_per_call": s["tN_ms"] * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8 keys, f32 LUT/accumulate, f64 alpha epilogue",
+            "data": s["data"], "config": {"workload": s["workload"], "step": s["step"],
+                                          "parallelism": f"rows x{ctx.world}"},
+            "roofline": {"bound": "lds", "achieved": s["tN_gbs"], "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
+                         "frac": round(kb / (s["tN_ms"] * 1e-3) / 1e9 / (ctx.world * peak), 4), "traffic": None},
+            "gpu_launches": 2 * s["steps"], "c5_strong": s,
+            "e2e": {"value": s["tN_gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "device-resident x and y; the collectives are inside the step"}}
+
+
+# ------------------------------------------------------------ reference points
+
+
+def comparators(bq, layer, x_h, m, n, beta, b, mu, kb, dev, calls=200):
     """The paper's comparison points on this GPU (Table IV
     analog), device-timed per call with rotating copies > 2x L2: cuBLAS dense
     GEMV on the dequantized weights (fp32 and bf16), the reference's
@@ -477,23 +906,20 @@ def comparators(bq, layer, w, x_h, m, n, beta, b, mu, kb, dev, calls=200):
                                                         stream=torch.cuda.current_stream().cuda_stream))
                  for j in range(calls)])
     out["bandwidth_probe_gpu"] = {"us_per_call": round(us, 3), "key_gbs": round(kb / (us * 1e-6) / 1e9, 1),
-                                  "what": "streaming read of the packed sign words (the key-stream roofline)"}
+                                  "what": "the reference's gemm_bandwidth_probe as a GPU kernel (one multiply-add "
+                                          "per packed sign word)"}
     return out
-
-
-# ------------------------------------------------------------ CPU reference
 
 
 def cpu_baseline(config, keys, alpha, x, m, n, beta, mu, b, seconds):
     """The reference's own biqgemm (oracle/_ref) on this host, single thread
     and all threads; bench_cli protocol (warmup, median of repeats)."""
-    from oracle.oracle import Port, Reference, cpu_threads, reference
+    from oracle.oracle import cpu_threads, reference
 
     kb = key_bytes(m, n, beta, mu)
     ref = reference()
-    kind = "reference" if ref is not None else "port"
     if ref is None:
-        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "port",
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref missing; no timing"}
     keys32 = np.ascontiguousarray(keys, np.uint32)
     nthreads = cpu_threads()
@@ -506,24 +932,40 @@ def cpu_baseline(config, keys, alpha, x, m, n, beta, mu, b, seconds):
         med = float(np.median(secs))
         detail[str(threads)] = {"median_us": med * 1e6, "repeats": reps, "checksum": cs}
         if best is None or med < best[0]:
-            best = (med, threads, reps)
-    med, threads, reps = best
-    return {"value": round(kb / med / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": kind,
-            "us_per_call": med * 1e6,
+            best = (med, threads, reps, cs)
+    med, threads, reps, cs = best
+    return {"value": round(kb / med / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+            "us_per_call": med * 1e6, "checksum": cs, "cpu_model": cpu_model(),
             "sample": f"{config}: median of {reps} reference biqgemm calls (plan_tiles budget max(32KiB, 2^mu*b*4B)), "
                       f"threads in {{1,{nthreads}}}, best shown",
             "per_threads": detail, "host_threads": nthreads}
 
 
+def reference_checksum_parity(bq, layer, x, cpu):
+    """In the same run: the GPU exact path's checksum (fp64 sequential sum of
+    y, the shim's definition) must equal the reference's bit for bit, and the
+    fast path's y is within the fp32 contract of the exact y."""
+    if cpu.get("checksum") is None:
+        return None
+    y_exact = layer.forward(x, exact=True)
+    y_fast = layer.forward(x)
+    ce, cf = seq_sum(y_exact), seq_sum(y_fast)
+    rel = float(np.linalg.norm(y_fast.astype(np.float64) - y_exact) / np.linalg.norm(y_exact.astype(np.float64)))
+    return {"reference_checksum": cpu["checksum"], "gpu_exact_checksum": ce, "exact_bitwise_equal": ce == cpu["checksum"],
+            "gpu_fast_checksum": cf, "fast_rel_fro_vs_exact": rel}
+
+
 def run_reference(args):
+    """The reference's CPU biqgemm (oracle/_ref) on the host cores; nothing
+    from this repo's package is imported or loaded."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    import paper_2005_09904_b200.biqgemm as bq  # host RNG only (pinned == reference RNG)
-    from oracle.oracle import reference
+    from oracle.oracle import cpu_threads, reference
 
     ref = reference()
-    m, n, beta, b, mu = CONFIGS[args.config]
+    cfg = args.config or "C2"
+    m, n, beta, b, mu = CONFIGS[cfg]
     if ref is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbqg_ref.so not built"}))
         return
@@ -531,8 +973,6 @@ def run_reference(args):
     x = ref.random_normal(n, b, SEED + 1)
     _, alpha, keys = ref.quantize_pack(w, beta, mu)
     kb = key_bytes(m, n, beta, mu)
-    from oracle.oracle import cpu_threads
-
     nthreads = cpu_threads()
     # per step: one reference call; pick the faster thread count on a probe
     best_t, best_s = 1, None
@@ -550,10 +990,11 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": total / steps * 1e3, "us_per_call": total / steps * 1e6,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 keys, f64 LUT/accumulate",
         "data": "synthetic (bench_cli generator)", "impl": "reference",
-        "config": {"workload": f"{args.config} m={m} n={n} q={beta} mu={mu} b={b}", "m": m, "n": n, "beta": beta,
+        "config": {"workload": f"{cfg} m={m} n={n} q={beta} mu={mu} b={b}", "m": m, "n": n, "beta": beta,
                    "mu": mu, "batch": b},
         "cpu_baseline": {"value": round(val, 5), "unit": "GB/s", "cores": best_t, "kind": "reference",
-                         "sample": f"{steps} reference biqgemm calls ({args.config}), threads={best_t} of {nthreads}"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{steps} reference biqgemm calls ({cfg}), threads={best_t} of {nthreads}"},
         "e2e": {"value": round(val, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "checksum": cs,
     }
@@ -563,21 +1004,24 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=50)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--steps", type=int, default=20, help="timed steps (grouped launches of --group calls)")
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-comparators", action="store_true", help="skip the cuBLAS / unpack / probe reference points")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the group-size sweep")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 strong-scaling leg")
+    ap.add_argument("--c5-steps", type=int, default=50)
+    ap.add_argument("--latency-calls", type=int, default=512)
     ap.add_argument("--batch", type=int, default=0, help="override the config's batch b (C4 sweep)")
-    ap.add_argument("--group", type=int, default=128, help="independent calls per grouped launch")
-    ap.add_argument("--e2e-group", type=int, default=512, help="calls per bqg_layers_forward_host call (e2e leg)")
-    ap.add_argument("--profile", action="store_true", help="for ncu: warm-up + one timed replay only, no JSON line")
+    ap.add_argument("--group", type=int, default=GROUP, help="independent calls per grouped launch (one step)")
+    ap.add_argument("--profile", action="store_true", help="for ncu: warm-up + one timed sequence only, no JSON line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
-        args.steps = min(args.steps, 500)  # a reference step is ~30 ms of CPU: keep the run within minutes
+        args.steps = min(args.steps, 500)  # a reference step is ~5-30 ms of CPU: keep the run within minutes
         run_reference(args)
     else:
         run_ours(args)

@@ -349,6 +349,27 @@ int bqg_biqgemm_sharded_f32(const uint8_t* d_keys_tiled_shard, const float* d_al
                             const bqg_collectives* coll, void* d_workspace, size_t workspace_bytes,
                             void* stream);
 
+/* A GROUP of row-sharded calls (the serving batch of bqg_biqgemm_grouped_f32,
+ * each layer row-sharded): one broadcast of all calls' x, the grouped kernel
+ * on this rank's rows of every call, one all-gather.
+ *   d_x: count x (x_rows x b) contiguous; rank 0's contents are broadcast.
+ *   d_y_gather: nranks x count x (R x b): block (r, i) holds rows
+ *     [r*R, r*R + rows_r) of call i's y (R from bqg_shard_rows), so call i's
+ *     y is the concatenation over r of the first rows_r rows of block (r, i).
+ * h_calls: HOST array of this rank's shards (keys tiled, alpha or NULL).
+ * Workspace: bqg_biqgemm_grouped_sharded_workspace_bytes(). */
+typedef struct bqg_shard_call {
+    const uint8_t* d_keys_tiled_shard;
+    const float* d_alpha_shard;
+} bqg_shard_call;
+size_t bqg_biqgemm_grouped_sharded_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta,
+                                                   unsigned mu, size_t count, int nranks);
+int bqg_biqgemm_grouped_sharded_f32(const bqg_shard_call* h_calls, size_t count, float* d_x,
+                                    size_t x_rows, float* d_y_gather, size_t m, size_t n, size_t b,
+                                    unsigned beta, unsigned mu, int rank, int nranks,
+                                    const bqg_collectives* coll, void* d_workspace,
+                                    size_t workspace_bytes, int pdl, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,12 @@ class Call(C.Structure):
     _fields_ = [("d_keys_tiled", vp), ("d_alpha", vp), ("d_x", vp), ("d_y", vp)]
 
 
+class ShardCall(C.Structure):
+    """bqg_shard_call: one entry of a grouped row-sharded launch (this rank's shard)."""
+
+    _fields_ = [("d_keys_tiled_shard", vp), ("d_alpha_shard", vp)]
+
+
 # name -> (restype, argtypes).  Every symbol declared in include/bqg_capi.h.
 SIGNATURES = {
     "bqg_status_string": (C.c_char_p, [i32]),
@@ -132,6 +138,9 @@ SIGNATURES = {
     "bqg_biqgemm_sharded_workspace_bytes": (sz, [sz, sz, sz, u32, u32, i32]),
     "bqg_biqgemm_sharded_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, i32, i32, P(Collectives), vp, sz,
                                       vp]),
+    "bqg_biqgemm_grouped_sharded_workspace_bytes": (sz, [sz, sz, sz, u32, u32, sz, i32]),
+    "bqg_biqgemm_grouped_sharded_f32": (i32, [vp, sz, vp, sz, vp, sz, sz, sz, u32, u32, i32, i32, P(Collectives), vp,
+                                              sz, i32, vp]),
 }
 
 

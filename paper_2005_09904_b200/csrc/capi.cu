@@ -1451,3 +1451,44 @@ extern "C" int bqg_biqgemm_sharded_f32(const uint8_t* d_keys_tiled_shard, const 
     // 3. the row blocks to every rank: the buffer's first m*b floats are y
     return coll->allgather(coll->ctx, y_mine, d_y_gather, R * b * sizeof(float), stream);
 }
+
+extern "C" size_t bqg_biqgemm_grouped_sharded_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta,
+                                                              unsigned mu, size_t count, int nranks) {
+    size_t R = 0;
+    if (bqg_shard_rows(m, nranks, 0, nullptr, nullptr, &R) != BQG_OK) return 0;
+    return bqg_biqgemm_grouped_workspace_bytes(std::min(R, m), n, b, beta, mu, count);
+}
+
+extern "C" int bqg_biqgemm_grouped_sharded_f32(const bqg_shard_call* h_calls, size_t count, float* d_x, size_t x_rows,
+                                               float* d_y_gather, size_t m, size_t n, size_t b, unsigned beta,
+                                               unsigned mu, int rank, int nranks, const bqg_collectives* coll,
+                                               void* d_ws, size_t ws_bytes, int pdl, void* stream) {
+    size_t lo = 0, hi = 0, R = 0;
+    int s = bqg_shard_rows(m, nranks, rank, &lo, &hi, &R);
+    if (s) return s;
+    if (!coll || !coll->broadcast || !coll->allgather)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: collectives missing");
+    if (!d_x || !d_y_gather || (count && !h_calls))
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null pointer");
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    if (count == 0) return BQG_OK;
+    const size_t xs = x_rows * b, block = R * b;
+    // 1. every call's x from rank 0, one broadcast of the contiguous batch
+    s = coll->broadcast(coll->ctx, d_x, count * xs * sizeof(float), 0, stream);
+    if (s) return s;
+    // 2. the group on this rank's rows: call i -> block (rank, i) of the gather buffer
+    float* y_mine = d_y_gather + static_cast<size_t>(rank) * count * block;
+    if (hi > lo) {
+        std::vector<bqg_call> calls(count);
+        for (size_t i = 0; i < count; ++i) {
+            if (!h_calls[i].d_keys_tiled_shard)
+                return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null keys in call %zu", i);
+            calls[i] = {h_calls[i].d_keys_tiled_shard, h_calls[i].d_alpha_shard, d_x + i * xs, y_mine + i * block};
+        }
+        s = bqg_biqgemm_grouped_f32(calls.data(), count, x_rows, hi - lo, n, b, beta, mu, d_ws, ws_bytes, pdl, stream);
+        if (s) return s;
+    }
+    // 3. the rank blocks to every rank
+    return coll->allgather(coll->ctx, y_mine, d_y_gather, count * block * sizeof(float), stream);
+}

@@ -276,3 +276,66 @@ class ShardedLinear:
         if self.layer is not None:
             self.layer.close()
             self.layer = None
+
+
+class ShardedGroup:
+    """A group of row-sharded layers that share (m, n, beta, mu) -- the
+    serving batch of the grouped entry, every layer row-sharded -- run as ONE
+    bqg_biqgemm_grouped_sharded_f32: one broadcast of all inputs, the grouped
+    kernel on this rank's rows of every layer, one all-gather of all outputs."""
+
+    def __init__(self, shards: list):
+        from . import biqgemm as bq
+
+        if not shards:
+            raise ValueError("ShardedGroup: no layers")
+        s0 = shards[0]
+        for s in shards:
+            if (s.m, s.n, s.beta, s.mu, s.rank, s.world) != (s0.m, s0.n, s0.beta, s0.mu, s0.rank, s0.world):
+                raise ValueError("ShardedGroup: layers must share (m, n, beta, mu) and the rank layout")
+        self.bq = bq
+        self.shards = list(shards)
+        self.m, self.n, self.beta, self.mu = s0.m, s0.n, s0.beta, s0.mu
+        self.rank, self.world, self.plan, self.device = s0.rank, s0.world, s0.plan, s0.device
+        self.coll_provider = s0.coll_provider
+        self._arr = (bq._capi.ShardCall * len(self.shards))()
+        for i, s in enumerate(self.shards):
+            if s.layer is not None:
+                self._arr[i] = bq._capi.ShardCall(s.layer.device_tiled_keys, s.layer.device_alpha)
+        self._ws = {}
+
+    def __len__(self):
+        return len(self.shards)
+
+    def gather_buffer(self, b: int) -> torch.Tensor:
+        """[world, count, R, b]: block (r, i) holds rank r's rows of layer i."""
+        return torch.empty((self.world, len(self), self.plan.max_rows, b), dtype=torch.float32, device=self.device)
+
+    def assemble(self, y_gather: torch.Tensor) -> torch.Tensor:
+        """[count, m, b] from the gather buffer (rank blocks concatenated)."""
+        w, c, R, b = y_gather.shape
+        return y_gather.permute(1, 0, 2, 3).reshape(c, w * R, b)[:, : self.m]
+
+    def forward_device(self, x: torch.Tensor, y_gather: torch.Tensor, pdl: bool = False, stream=None) -> torch.Tensor:
+        """x: [count, n, b] device batch (rank 0's contents are broadcast into
+        it); returns assemble(y_gather)."""
+        bq = self.bq
+        count, x_rows, b = x.shape
+        if count != len(self):
+            raise ValueError(f"ShardedGroup: {count} inputs for {len(self)} layers")
+        if not (x.dtype == torch.float32 and x.is_contiguous() and x.device == self.device):
+            raise ValueError("ShardedGroup: x must be a contiguous float32 tensor on this rank's device")
+        if tuple(y_gather.shape) != (self.world, count, self.plan.max_rows, b) or not y_gather.is_contiguous():
+            raise ValueError("ShardedGroup: y_gather must come from gather_buffer(b)")
+        if isinstance(self.coll_provider, TorchCollectives):
+            self.coll_provider.register(x, y_gather)
+        if b not in self._ws:
+            self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_workspace_bytes(
+                self.m, self.n, b, self.beta, self.mu, count, self.world)), device=self.device)
+        ws = self._ws[b]
+        coll = self.coll_provider.collectives()
+        bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
+            C.cast(self._arr, C.c_void_p), count, x.data_ptr(), x_rows, y_gather.data_ptr(), self.m, self.n, b,
+            self.beta, self.mu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
+            bq._stream(stream)))
+        return self.assemble(y_gather)

@@ -177,6 +177,61 @@ def _native_worker_body(rank, world, m, n, beta, b, out_q):
         sh.close()
 
 
+def _grouped_worker(rank, world, port, m, n, beta, count, out_q):
+    """One rank of the grouped row-sharded C-ABI call
+    (bqg_biqgemm_grouped_sharded_f32) on one GPU with gloo collectives."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2005_09904_b200.biqgemm as bq
+        from paper_2005_09904_b200.sharded import ShardedGroup, ShardedLinear, TorchCollectives
+
+        coll = TorchCollectives()
+        ws_ = [bq.random_uniform(m, n, 100 + i) for i in range(count)]
+        shards = [ShardedLinear.from_weights(w, beta, 8, rank, world, coll) for w in ws_]
+        grp = ShardedGroup(shards)
+        x_h = np.stack([bq.random_normal(n, 1, 200 + i) for i in range(count)])
+        x = torch.from_numpy(x_h).cuda() if rank == 0 else torch.zeros((count, n, 1), device="cuda")
+        yg = grp.gather_buffer(1)
+        y = grp.forward_device(x, yg).cpu().numpy()
+        ok, diff = True, 0.0
+        for i, w in enumerate(ws_):
+            full = bq.PackedLinear.from_weights(w, beta, 8)
+            y_full = full.forward(x_h[i])
+            ok = ok and bool(np.array_equal(y[i], y_full))
+            diff = max(diff, float(np.abs(y[i] - y_full).max()))
+            full.close()
+        for s in shards:
+            s.close()
+        out_q.put((rank, ok, diff))
+    except Exception as e:
+        out_q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,m,n,beta,count", [(2, 4096, 4096, 3, 6), (3, 1000, 777, 2, 5)])
+def test_native_grouped_sharded_single_gpu_gloo(cuda, world, m, n, beta, count):
+    """bqg_biqgemm_grouped_sharded_f32 (one broadcast of the x batch, the
+    grouped kernel on each rank's rows, one all-gather): every layer's
+    assembled y == its unsharded y, bit for bit, on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_grouped_worker, args=(r, world, portn, m, n, beta, count, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, diff in res:
+        assert ok, f"rank {rank}: {diff}"
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,m,n,beta,b", [(2, 4096, 4096, 3, 1), (3, 1000, 777, 2, 1), (2, 3000, 1024, 2, 4)])
 def test_native_sharded_single_gpu_gloo(cuda, world, m, n, beta, b):
