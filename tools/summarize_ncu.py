@@ -73,16 +73,18 @@ def main():
     summary = json.loads(sp.read_text()) if sp.exists() else {}
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     L = [f"# ncu evidence, round {tag}", "",
-         "Captured with tools/profile_round.sh under gpurun on one B200: `ncu --set full --clock-control none "
-         "--import-source on -k regex:biqgemm_stream_kernel -s 2 -c 1` of `python bench.py --config <C> --profile "
-         "--steps 512 --warmup 3` (one grouped launch = 128 independent calls), and the launch list "
-         "(`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`, cold-cache, serialised: "
-         "compare shares, not absolutes).", ""]
+         "Captured under gpurun on one B200 (tools/profile_r2.sh): `ncu --set full --clock-control none "
+         "--import-source on -k regex:<kernel> -s <skip> -c 1` of `python bench.py --config <C> --profile --steps 4 "
+         "--warmup 3` (a grouped launch = one bench step = 128 independent calls), and the launch lists "
+         "(`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`; "
+         "cold-cache and serialised: compare shares, not absolutes).", ""]
     for cfg in cfgs:
         m, n, beta, b, mu = CONFIGS[cfg]
         kb = key_bytes(m, n, beta, mu)
         for rep, kname, calls in ((d / f"full_{cfg}.ncu-rep", "biqgemm_stream_kernel", 128),
-                                  (d / f"lat_{cfg}.ncu-rep", "biqgemm_latency_kernel", 1)):
+                                  (d / f"full_tex_{cfg}.ncu-rep", "biqgemm_tex_kernel", 128),
+                                  (d / f"lat_{cfg}.ncu-rep", "biqgemm_latency_kernel", 1),
+                                  (d / f"full_lat_{cfg}.ncu-rep", "biqgemm_latency_kernel", 1)):
             if not rep.exists():
                 continue
             for k in raw(rep):
@@ -117,9 +119,13 @@ def main():
                 if calls > 1:
                     summary[cfg] = {"dram_bytes_per_launch": rd + wr, "calls_per_launch": calls,
                                     "algorithmic_bytes_per_launch": alg, "duration_us_ncu": dur / 1e3,
-                                    "kernel": name[:100], "round": tag}
+                                    "kernel": name[:100], "round": tag,
+                                    "dram_bytes_per_call": (rd + wr) / calls,
+                                    "source": f"profiles/ncu_{tag}.md ({rep.name}: ncu --set full, one launch)"}
         # b >= 2 forms: the two-kernel fast form (tools/fast_sweep.py under ncu)
         fp = d / f"fast_{cfg}.ncu-rep"
+        if not fp.exists():
+            fp = d / f"full_fast_{cfg}.ncu-rep"
         if fp.exists():
             G = (n + mu - 1) // mu
             lds_alg = 4 * beta * m * G * b  # LUT bytes gathered
@@ -146,7 +152,7 @@ def main():
             shutil.copy(lp, PROF / f"ncu_launches_{tag}_{cfg}.csv")
             agg = launch_shares(lp)
             tot = sum(a[1] for a in agg.values()) or 1
-            L += [f"### {cfg} launch list (whole bench --profile run, incl. setup kernels)", "",
+            L += [f"### {cfg} launch list (whole bench run under ncu, incl. setup kernels)", "",
                   "| kernel | launches | time us | share | DRAM read MB |", "|---|---|---|---|---|"]
             for nm, (c, t, rb) in sorted(agg.items(), key=lambda x: -x[1][1]):
                 L.append(f"| `{nm}` | {c} | {t / 1e3:.1f} | {t / tot * 100:.1f}% | {rb / 1e6:.1f} |")
