@@ -337,9 +337,12 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
 #endif
 constexpr int kNW = BQG_FAST_NW;
 
+#ifndef BQG_FAST_R4
+#define BQG_FAST_R4 6
+#endif
 template <int BT>
 constexpr int stages_for() {
-    return BT == 1 ? 6 : (BT == 2 ? 4 : 6);
+    return BT == 1 ? 6 : (BT == 2 ? 4 : BQG_FAST_R4);
 }
 
 template <int MU, int BT>

@@ -35,14 +35,22 @@ namespace bqg {
 
 // Per-CTA timeline (BQG_DEBUG_FLAGS & 2): globaltimer ns at start, after the
 // cluster rendezvous, after griddepcontrol.wait, LUT built, gather done,
-// partials pushed, y stored.  Off in production.
-__device__ unsigned long long g_timeline_lat[1024][8];
+// partials pushed, y stored, prologue barrier; thread 0: x loaded, its DFS
+// done, first key piece landed, its last chunk gathered.  Off in production.
+__device__ unsigned long long g_timeline_lat[1024][12];
 
 namespace {
 
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The timer read is ordered after v is available (v is an asm input).
+__device__ __forceinline__ unsigned long long gtime_after(float v) {
+    unsigned long long t;
+    asm volatile("{\n\t.reg .f32 d;\n\tmov.f32 d, %1;\n\tmov.u64 %0, %%globaltimer;\n}" : "=l"(t) : "f"(v));
     return t;
 }
 
@@ -98,7 +106,7 @@ struct LDfs {
 // gb*256 + lane*8 .. +7, zero past x_rows) into the LUT half at col.
 template <int NBW>
 __device__ __forceinline__ void build_share(int which, uint32_t col, const float* __restrict__ x, long long x_rows,
-                                            int gb, int lane) {
+                                            int gb, int lane, unsigned long long* tl) {
     float xv[kMU], s[kMU];
     const long long r0 = static_cast<long long>(gb) * 32 * kMU + lane * kMU;
     if (r0 + kMU <= x_rows && (reinterpret_cast<uintptr_t>(x + r0) & 15) == 0) {
@@ -113,9 +121,11 @@ __device__ __forceinline__ void build_share(int which, uint32_t col, const float
     float e0 = 0.0f;
 #pragma unroll
     for (int t = 0; t < kMU; ++t) e0 = __fsub_rn(e0, xv[t]);
+    if (tl) tl[8] = gtime_after(e0);  // x has arrived
 #pragma unroll
     for (int t = 0; t < kMU; ++t) s[t] = 2.0f * xv[t];
     LDfs<0, 0, 7 - Log2<NBW>::value>::node(e0, s, col, which);
+    if (tl) tl[9] = gtime();
 }
 
 // ---- gather (identical arithmetic to biqgemm_stream.cu) -------------------
@@ -297,8 +307,9 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
         const int b = warp / (kLB / bpc), which = warp - b * (kLB / bpc);
         const uint32_t col = lut_abs + static_cast<uint32_t>(b) * 128u + static_cast<uint32_t>(lane) * 4u;
         const int gb = s_rank * bpc + b;
-        if (bpc == 1) build_share<16>(which, col, A.x, A.x_rows, gb, lane);
-        else build_share<8>(which, col, A.x, A.x_rows, gb, lane);
+        unsigned long long* tlw = (tl && warp == 0) ? g_timeline_lat[blockIdx.x] : nullptr;
+        if (bpc == 1) build_share<16>(which, col, A.x, A.x_rows, gb, lane, tlw);
+        else build_share<8>(which, col, A.x, A.x_rows, gb, lane, tlw);
     }
     __syncthreads();
     if (tl) g_timeline_lat[blockIdx.x][3] = gtime();
@@ -307,10 +318,12 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
     for (int q = warp; q < nchunk; q += kLW) {
         const int b = q / nchunk_b, c = q - b * nchunk_b;
         mbar_wait(&kbar[b * npb + c / kPieceChunks], 0);
+        if (tl && q == 0) g_timeline_lat[blockIdx.x][10] = gtime();
         const uint32_t ka = keys_at + static_cast<uint32_t>(q) * 1024u;
         const float P = b == 0 ? gather_chunk_l<0>(ka, lane, rot, rank_bits) : gather_chunk_l<128>(ka, lane, rot, rank_bits);
         psum[q * 32 + lane] = P;
     }
+    if (tl) g_timeline_lat[blockIdx.x][11] = gtime();
     mbar_wait(abar, 0);
     __syncthreads();
     if (tl) g_timeline_lat[blockIdx.x][4] = gtime();
@@ -490,7 +503,7 @@ bool plan_latency(const QueryParams& p, LatArgs& A, int& nclusters) {
 }  // namespace bqg
 
 extern "C" int bqg_debug_timeline_latency(unsigned long long* out, int rows) {
-    return cudaMemcpyFromSymbol(out, bqg::g_timeline_lat, sizeof(unsigned long long) * 8 * (rows < 1024 ? rows : 1024)) ==
+    return cudaMemcpyFromSymbol(out, bqg::g_timeline_lat, sizeof(unsigned long long) * 12 * (rows < 1024 ? rows : 1024)) ==
                    cudaSuccess
                ? 0
                : 2;
