@@ -216,9 +216,21 @@ uint64_t bqo_build_lut_block_f32(const float* x, size_t x_rows, size_t b,
  * (criterion 7), so the restatement uses one tile covering all groups.
  * keys: beta x m x G (u32).  counters[0..2] = build ops, lookups,
  * accumulate ops (kernel.hpp:179-180). */
+int bqo_biqgemm_ex_f32(const uint32_t* keys, const float* alpha, size_t m, size_t n,
+                       unsigned beta, unsigned mu, const float* x, size_t x_rows,
+                       size_t b, int naive, float* y, uint64_t* counters);
+
 int bqo_biqgemm_f32(const uint32_t* keys, const float* alpha, size_t m, size_t n,
                     unsigned beta, unsigned mu, const float* x, size_t x_rows,
                     size_t b, float* y, uint64_t* counters) {
+    return bqo_biqgemm_ex_f32(keys, alpha, m, n, beta, mu, x, x_rows, b, 0, y, counters);
+}
+
+/* The same with KernelOptions::builder (kernel.hpp:51,158): naive != 0
+ * builds every table with build_lut_naive (lut.hpp:31-43) instead of the DP. */
+int bqo_biqgemm_ex_f32(const uint32_t* keys, const float* alpha, size_t m, size_t n,
+                       unsigned beta, unsigned mu, const float* x, size_t x_rows,
+                       size_t b, int naive, float* y, uint64_t* counters) {
     if (mu < 1 || mu > 16 || beta == 0) return BQO_EINVAL;
     const size_t groups = (n + mu - 1) / mu;
     if ((size_t)mu * groups < x_rows) return BQO_EINVAL; /* kernel.hpp:132-134 */
@@ -228,7 +240,7 @@ int bqo_biqgemm_f32(const uint32_t* keys, const float* alpha, size_t m, size_t n
     double* acc = (double*)calloc((size_t)beta * m * b, sizeof(double));
     if (!lut || !acc) { free(lut); free(acc); return BQO_EINVAL; }
     const uint64_t ops = bqo_build_lut_block_f64(x, x_rows, b, 0, groups, mu,
-                                                 key_major, 0, lut);
+                                                 key_major, naive, lut);
     for (unsigned i = 0; i < beta; ++i) {
         const uint32_t* kp = keys + (size_t)i * m * groups;
         double* ai = acc + (size_t)i * m * b;

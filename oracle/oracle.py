@@ -51,6 +51,7 @@ class Port:
             "bqo_build_lut_block_f64": (u64, [vp, sz, sz, sz, sz, u32, i32, i32, vp]),
             "bqo_build_lut_block_f32": (u64, [vp, sz, sz, sz, sz, u32, i32, vp]),
             "bqo_biqgemm_f32": (i32, [vp, vp, sz, sz, u32, u32, vp, sz, sz, vp, vp]),
+            "bqo_biqgemm_ex_f32": (i32, [vp, vp, sz, sz, u32, u32, vp, sz, sz, i32, vp, vp]),
             "bqo_gemm_dense_f32": (i32, [vp, sz, sz, vp, sz, vp]),
             "bqo_plan_tiles": (i32, [sz, sz, sz, u32, sz, sz, P(sz), P(sz)]),
             "bqo_frobenius_distance_f32": (f64, [vp, vp, sz]),
@@ -114,7 +115,7 @@ class Port:
         return out, ops
 
     # kernel.hpp:116-204
-    def biqgemm(self, keys, alpha, n, mu, x):
+    def biqgemm(self, keys, alpha, n, mu, x, naive=False):
         keys = np.ascontiguousarray(keys, np.uint32)
         beta, m, _ = keys.shape
         x = _f32(x)
@@ -122,7 +123,7 @@ class Port:
         y = np.empty((m, b), np.float32)
         cnt = np.zeros(3, np.uint64)
         a = None if alpha is None else _f32(alpha)
-        st = self.L.bqo_biqgemm_f32(_p(keys), _p(a), m, n, beta, mu, _p(x), x_rows, b, _p(y), _p(cnt))
+        st = self.L.bqo_biqgemm_ex_f32(_p(keys), _p(a), m, n, beta, mu, _p(x), x_rows, b, int(naive), _p(y), _p(cnt))
         if st != 0:
             raise ValueError("biqgemm: invalid argument")
         return y, dict(lut_build_ops=int(cnt[0]), lookups=int(cnt[1]), accumulate_ops=int(cnt[2]))
@@ -163,6 +164,7 @@ class Reference:
             "ref_pack_keys": (i32, [vp, sz, sz, u32, vp]),
             "ref_build_lut_block": (i32, [vp, sz, sz, sz, sz, u32, i32, i32, vp, P(u64)]),
             "ref_biqgemm_f32": (i32, [vp, vp, sz, sz, u32, u32, vp, sz, sz, sz, sz, sz, sz, vp, vp]),
+            "ref_biqgemm_builder_f32": (i32, [vp, vp, sz, sz, u32, u32, vp, sz, sz, sz, sz, sz, sz, i32, vp, vp]),
             "ref_time_biqgemm_f32": (i32, [vp, vp, sz, sz, u32, u32, vp, sz, sz, i32, i32, vp, P(f64)]),
             "ref_gemm_dense_dequant_f32": (i32, [vp, vp, sz, sz, u32, vp, sz, vp]),
             "ref_save_bqgm": (i32, [vp, sz, sz, u32, u32, vp, P(sz)]),
@@ -214,7 +216,7 @@ class Reference:
                                             C.byref(ops)))
         return out, ops.value
 
-    def biqgemm(self, keys, alpha, n, mu, x, t_w=None, t_h=None, threads=1, budget=0):
+    def biqgemm(self, keys, alpha, n, mu, x, t_w=None, t_h=None, threads=1, budget=0, naive=False):
         keys = np.ascontiguousarray(keys, np.uint32)
         beta, m, G = keys.shape
         x = _f32(x)
@@ -222,8 +224,8 @@ class Reference:
         y = np.empty((m, b), np.float32)
         st = np.zeros(7, np.float64)
         a = None if alpha is None else _f32(alpha)
-        self._ck(self.L.ref_biqgemm_f32(_p(keys), _p(a), m, n, beta, mu, _p(x), x_rows, b, t_w or G, t_h or m,
-                                        threads, budget, _p(y), _p(st)))
+        self._ck(self.L.ref_biqgemm_builder_f32(_p(keys), _p(a), m, n, beta, mu, _p(x), x_rows, b, t_w or G, t_h or m,
+                                                threads, budget, int(naive), _p(y), _p(st)))
         return y, dict(lut_build_ops=int(st[0]), lookups=int(st[1]), accumulate_ops=int(st[2]), fma_ops=int(st[3]),
                        build_seconds=st[4], query_seconds=st[5], replace_seconds=st[6])
 

@@ -158,10 +158,26 @@ int ref_build_lut_block(const float* x, std::size_t x_rows, std::size_t b,
 
 // biqgemm (alpha != NULL) or biqgemm_plane semantics (alpha == NULL, beta == 1).
 // stats: [build_ops, lookups, accumulate_ops, fma_ops] + [build_s, query_s, replace_s]
+int ref_biqgemm_builder_f32(const std::uint32_t* keys, const float* alpha, std::size_t m,
+                            std::size_t n, unsigned beta, unsigned mu, const float* x,
+                            std::size_t x_rows, std::size_t b, std::size_t t_w, std::size_t t_h,
+                            std::size_t threads, std::size_t budget, int naive, float* y,
+                            double* stats);
+
 int ref_biqgemm_f32(const std::uint32_t* keys, const float* alpha, std::size_t m,
                     std::size_t n, unsigned beta, unsigned mu, const float* x,
                     std::size_t x_rows, std::size_t b, std::size_t t_w, std::size_t t_h,
                     std::size_t threads, std::size_t budget, float* y, double* stats) {
+    return ref_biqgemm_builder_f32(keys, alpha, m, n, beta, mu, x, x_rows, b, t_w, t_h, threads,
+                                   budget, 0, y, stats);
+}
+
+// The same with KernelOptions::builder = Naive when naive != 0.
+int ref_biqgemm_builder_f32(const std::uint32_t* keys, const float* alpha, std::size_t m,
+                            std::size_t n, unsigned beta, unsigned mu, const float* x,
+                            std::size_t x_rows, std::size_t b, std::size_t t_w, std::size_t t_h,
+                            std::size_t threads, std::size_t budget, int naive, float* y,
+                            double* stats) {
     try {
         auto model = make_model(keys, alpha, m, n, beta, mu);
         Matrix<float> X(x_rows, b, std::vector<float>(x, x + x_rows * b));
@@ -169,6 +185,7 @@ int ref_biqgemm_f32(const std::uint32_t* keys, const float* alpha, std::size_t m
         KernelOptions opts;
         opts.threads = threads;
         opts.budget_bytes = budget;
+        if (naive) opts.builder = LutBuilder::Naive;
         Matrix<float> Y = alpha ? biqgemm::biqgemm(model, X, TileShape{t_w, t_h}, &st, opts)
                                 : biqgemm_plane(model.keys[0], X, TileShape{t_w, t_h}, &st, opts);
         std::memcpy(y, Y.data(), sizeof(float) * m * b);

@@ -280,6 +280,32 @@ void kernel_tests() {
         auto ref = gemm_dense(dequantize(q), x);
         CHECK(frobenius_distance(y, ref) / frobenius_norm(ref) < 1e-4);
     }
+    {  // KernelOptions::builder (kernel.hpp:51,158): Naive = 2^mu*mu build ops per table on the exact
+       // path; a copy of a model starts without a device copy (its own keys/alphas are used)
+        auto w = Matrix<float>::random_uniform(64, 96, 51);
+        auto model = pack_linear(quantize_greedy(w, 2), 6);
+        auto x = Matrix<float>::random_normal(96, 2, 52);
+        KernelOptions naive;
+        naive.builder = LutBuilder::Naive;
+        KernelOptions ex;
+        ex.exact = true;
+        KernelStats sn, sd;
+        auto yn = biqgemm::biqgemm(model, x, TileShape{4, 8}, &sn, naive);
+        auto yd = biqgemm::biqgemm(model, x, TileShape{4, 8}, &sd, ex);
+        const std::uint64_t G = model.keys[0].groups;
+        CHECK(sn.ops.lut_build_ops == 64ull * 6 * G * 2);
+        CHECK(sd.ops.lut_build_ops == (64ull + 6 - 1) * G * 2);
+        CHECK(frobenius_distance(yn, yd) <= 1e-6 * frobenius_norm(yd));
+        CHECK(sn.build_seconds > 0 && sn.query_seconds > 0);
+        auto copy = model;
+        for (auto& a : copy.alphas) std::fill(a.begin(), a.end(), 0.0f);
+        auto yz = biqgemm::biqgemm(copy, x, TileShape{1, 1});
+        for (std::size_t i = 0; i < yz.rows(); ++i) CHECK(yz(i, 0) == 0.0f && yz(i, 1) == 0.0f);
+        CHECK(frobenius_norm(biqgemm::biqgemm(model, x, TileShape{1, 1})) > 0.0);
+        // biqgemm_plane keeps the key matrix's device copy: same answer on reuse
+        auto y1 = biqgemm_plane(model.keys[0], x, TileShape{1, 1});
+        CHECK(biqgemm_plane(model.keys[0], x, TileShape{2, 2}) == y1);
+    }
     {  // :108-134 + acceptance criterion 7: bitwise invariance over tiles/workers
         std::mt19937_64 rng(0x5EED);
         for (int rep = 0; rep < 10; ++rep) {

@@ -5,7 +5,8 @@ unmodified reference headers compiled by oracle/Makefile).  Run here, where
     python tests/golden/make_golden.py
 
 Writes tests/golden/cases.npz (small randomized cases mirroring the
-reference's acceptance generators) and tests/golden/configs.npz +
+reference's acceptance generators), tests/golden/naive.npz (the same with
+KernelOptions::builder = Naive) and tests/golden/configs.npz +
 configs.json (the BASELINE configs' outputs/checksums on the bench_cli data,
 seeds 0x5EED / 0x5EED+1, bench_cli.cpp:106-109).
 """
@@ -108,8 +109,44 @@ def configs(ref):
     (HERE / "configs.json").write_text(json.dumps(meta, indent=1))
 
 
+def naive_cases(ref):
+    """KernelOptions::builder = Naive (kernel.hpp:51,158; lut.hpp:31-43): the
+    reference's y and counters with naive tables, next to its DP y."""
+    rng = np.random.Generator(np.random.PCG64(4321))
+    out = {}
+    idx = 0
+    for mu in (2, 3, 5, 8, 9, 11, 12):
+        for rep in range(2):
+            m = int(rng.integers(8, 200))
+            n = int(rng.integers(16, 400))
+            b = int(rng.integers(1, 5))
+            beta = int(rng.integers(1, 4))
+            wseed, xseed = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**63))
+            w = ref.random_uniform(m, n, wseed)
+            x = ref.random_normal(n, b, xseed)
+            _, alpha, keys = ref.quantize_pack(w, beta, mu)
+            y_naive, st = ref.biqgemm(keys, alpha, n, mu, x, naive=True)
+            y_dp, _ = ref.biqgemm(keys, alpha, n, mu, x)
+            p = f"n{idx}_"
+            out[p + "dims"] = np.array([m, n, b, beta, mu], np.uint64)
+            out[p + "keys"] = keys.astype(np.uint16)
+            out[p + "alpha"] = alpha
+            out[p + "x"] = x
+            out[p + "y_naive"] = y_naive
+            out[p + "y_dp"] = y_dp
+            out[p + "counters"] = np.array([st["lut_build_ops"], st["lookups"], st["accumulate_ops"]], np.uint64)
+            idx += 1
+    out["count"] = np.array([idx])
+    np.savez_compressed(HERE / "naive.npz", **out)
+    print("naive cases:", idx)
+
+
 if __name__ == "__main__":
     r = Reference()
+    if "--naive-only" in sys.argv:
+        naive_cases(r)
+        sys.exit(0)
     if "--configs-only" not in sys.argv:
         cases(r)
+        naive_cases(r)
     configs(r)

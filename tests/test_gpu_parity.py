@@ -385,3 +385,63 @@ def test_both_fast_forms(cuda, flags):
     r = subprocess.run([sys.executable, str(Path(__file__).parent / "forms_check.py")], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_naive_builder_exact_path_vs_reference(bq, cuda):
+    """KernelOptions::builder = Naive runs the exact path with naive fp64
+    tables: y bit-identical to the reference run with LutBuilder::Naive
+    (tests/golden/naive.npz), counters with the naive law, and a real
+    build / query / replace phase split (kernel.hpp:156-159)."""
+    from paper_2005_09904_b200._capi import LUT_NAIVE, KernelStats
+
+    d = np.load(Path(__file__).resolve().parent / "golden" / "naive.npz")
+    for i in range(int(d["count"][0])):
+        c = {k[len(f"n{i}_"):]: d[k] for k in d.files if k.startswith(f"n{i}_")}
+        m, n, b, beta, mu = (int(v) for v in c["dims"])
+        keys = c["keys"].astype(np.uint16 if mu > 8 else np.uint8)
+        layer = bq.PackedLinear.from_keys(keys, c["alpha"], n, mu)
+        st = KernelStats()
+        y = layer.forward(c["x"], stats=st, builder=LUT_NAIVE)
+        assert np.array_equal(y, c["y_naive"]), f"case {i}"
+        assert [st.lut_build_ops, st.lookups, st.accumulate_ops] == [int(v) for v in c["counters"]]
+        assert st.build_seconds > 0 and st.query_seconds > 0 and st.replace_seconds > 0
+        assert np.array_equal(layer.forward(c["x"], exact=True), c["y_dp"])  # the Dp builder, exact path
+        layer.close()
+
+
+def test_exact_ex_entry_phase_split(bq, cuda):
+    """bqg_biqgemm_exact_ex_f32 on device buffers: builder choice and the
+    event-timed phase split; the fast path reports its build inside query."""
+    import ctypes as C
+
+    import torch
+    from paper_2005_09904_b200._capi import LUT_DP, LUT_NAIVE, KernelStats
+
+    m, n, b, beta, mu = 300, 700, 3, 2, 10
+    w = bq.random_uniform(m, n, 11)
+    x = bq.random_normal(n, b, 12)
+    layer = bq.PackedLinear.from_weights(w, beta, mu)
+    keys, alpha = layer.export()
+    kd = torch.from_numpy(keys.view(np.int16)).cuda()
+    ad = torch.from_numpy(alpha).cuda()
+    xd = torch.from_numpy(x).cuda()
+    ws = torch.empty(int(bq.lib.bqg_biqgemm_exact_workspace_bytes(m, n, b, beta, mu)), dtype=torch.uint8,
+                     device="cuda")
+    ys = {}
+    for builder in (LUT_DP, LUT_NAIVE):
+        yd = torch.empty((m, b), device="cuda")
+        st = KernelStats()
+        bq.check(bq.lib.bqg_biqgemm_exact_ex_f32(kd.data_ptr(), ad.data_ptr(), xd.data_ptr(), n, yd.data_ptr(), m, n,
+                                                b, beta, mu, builder, ws.data_ptr(), ws.numel(), C.byref(st), None))
+        G = (n + mu - 1) // mu
+        per = (1 << mu) * mu if builder == LUT_NAIVE else (1 << mu) + mu - 1
+        assert st.lut_build_ops == per * G * b
+        assert st.build_seconds > 0 and st.query_seconds > 0
+        ys[builder] = yd.cpu().numpy()
+    assert np.array_equal(ys[LUT_DP], layer.forward(x, exact=True))
+    fast = KernelStats()
+    layer2 = bq.PackedLinear.from_weights(w, beta, 8)
+    layer2.forward(x, stats=fast)
+    assert fast.build_seconds == 0 and fast.query_seconds > 0  # fused: the build runs inside the query kernel
+    layer.close()
+    layer2.close()
