@@ -37,7 +37,7 @@ namespace bqg {
 // cluster rendezvous, after griddepcontrol.wait, LUT built, gather done,
 // partials pushed, y stored, prologue barrier; thread 0: x loaded, its DFS
 // done, first key piece landed, its last chunk gathered.  Off in production.
-__device__ unsigned long long g_timeline_lat[1024][12];
+__device__ unsigned long long g_timeline_lat[1024][16];
 
 namespace {
 
@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
                 "l"(src), "r"(static_cast<uint32_t>(cn) * 1024u), "r"(smem_u32(&kbar[p])), "l"(pol)
                 : "memory");
         }
+        if ((A.debug & 2) && lane == 0 && blockIdx.x < 1024) g_timeline_lat[blockIdx.x][12] = gtime();
         // alpha: one plane per lane (lanes 31, 30, ...), all on abar
         {
             const uint32_t ab = static_cast<uint32_t>(rows) * 4u;
@@ -323,7 +324,11 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
         const float P = b == 0 ? gather_chunk_l<0>(ka, lane, rot, rank_bits) : gather_chunk_l<128>(ka, lane, rot, rank_bits);
         psum[q * 32 + lane] = P;
     }
-    if (tl) g_timeline_lat[blockIdx.x][11] = gtime();
+    if (tl) {
+        g_timeline_lat[blockIdx.x][11] = gtime();
+        for (int p = 0; p < npieces; ++p) mbar_wait(&kbar[p], 0);
+        g_timeline_lat[blockIdx.x][13] = gtime();
+    }
     mbar_wait(abar, 0);
     __syncthreads();
     if (tl) g_timeline_lat[blockIdx.x][4] = gtime();
@@ -503,7 +508,7 @@ bool plan_latency(const QueryParams& p, LatArgs& A, int& nclusters) {
 }  // namespace bqg
 
 extern "C" int bqg_debug_timeline_latency(unsigned long long* out, int rows) {
-    return cudaMemcpyFromSymbol(out, bqg::g_timeline_lat, sizeof(unsigned long long) * 12 * (rows < 1024 ? rows : 1024)) ==
+    return cudaMemcpyFromSymbol(out, bqg::g_timeline_lat, sizeof(unsigned long long) * 16 * (rows < 1024 ? rows : 1024)) ==
                    cudaSuccess
                ? 0
                : 2;

@@ -29,12 +29,12 @@ fn.argtypes = [C.c_void_p, C.c_int]
 for i in range(30):
     bq.biqgemm_device(copies[i % NC], al, x, y, m, n, beta, mu, ws, pdl=True)
 torch.cuda.synchronize()
-t = np.zeros((1024, 12), np.uint64)
+t = np.zeros((1024, 16), np.uint64)
 fn(t.ctypes.data, 1024)
 t = t[t[:, 0] > 0].astype(np.int64)
 t0v = t[:, 0].min()
 names = ["start", "cluster_arrive", "pdl_wait", "lut_built", "gathered", "pushed", "y_stored", "syncthreads",
-         "w0_x_loaded", "w0_dfs_done", "w0_keys_1st", "w0_gathered"]
+         "w0_x_loaded", "w0_dfs_done", "w0_keys_1st", "w0_gathered", "keys_issued", "keys_all_landed"]
 print(f"{cfg}: {len(t)} CTAs (last call of a 30-call PDL chain)")
 for i, nm in enumerate(names):
     v = t[:, i] - t0v
