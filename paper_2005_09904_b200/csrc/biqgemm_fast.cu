@@ -463,7 +463,8 @@ FastPlan make_plan(long long m, long long groups, int beta, long long b, int mu,
 size_t fast_workspace_bytes(long long m, long long groups, int beta, long long b) {
     const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
     const long long BT = pick_bt(b), bpad = (b + BT - 1) / BT * BT;  // column tiles are written whole
-    return static_cast<size_t>(NB) * beta * MT * 32 * std::max(b, bpad) * sizeof(float);
+    // the counters of the grouped forms first, then the partials of any form
+    return kTexCounterBytes + static_cast<size_t>(NB) * beta * MT * 32 * std::max(b, bpad) * sizeof(float);
 }
 
 int plan_cpb(long long m, long long groups, int beta, long long b, int num_sms) {
@@ -520,7 +521,7 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
     // than the stream form's (beta x the partials).
     if (!(debug_flags & (128 | 8192 | 65536)) && stream_supported(mu, p.beta, p.b)) {
         const StreamCall call{p.keys, p.alpha, p.x, p.y};
-        return launch_biqgemm_stream(&call, 1, p.x_rows, p.m, p.G, p.beta, p.partial, pdl, stream);
+        return launch_biqgemm_stream(&call, 1, p.x_rows, p.m, p.G, p.beta, p.ws, pdl, stream);
     }
     const FastPlan plan = make_plan(p.m, p.G, p.beta, p.b, mu, sms);
     const int bt = pick_bt(p.b);

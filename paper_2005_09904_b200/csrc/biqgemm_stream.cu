@@ -588,7 +588,7 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
 #define BQG_STREAM_STAGE_KB 16
 #endif
     A.ups = std::max(1, BQG_STREAM_STAGE_KB / beta);  // ~16 KiB ring stages (TMA bulk copies)
-    A.partial = ws;
+    A.partial = ws + kTexCounterBytes / sizeof(float);  // the counters stay the texture form's
     for (int done = 0; done < count; done += kStreamMaxGroup) {
         A.ncalls = std::min(kStreamMaxGroup, count - done);
         for (int i = 0; i < A.ncalls; ++i) A.calls[i] = calls[done + i];

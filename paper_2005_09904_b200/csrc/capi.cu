@@ -446,7 +446,8 @@ bqg::QueryParams make_params(const uint8_t* keys, const float* alpha, const floa
     p.alpha = alpha;
     p.x = x;
     p.y = y;
-    p.partial = static_cast<float*>(ws);
+    p.ws = static_cast<float*>(ws);
+    p.partial = p.ws + bqg::kTexCounterBytes / sizeof(float);
     p.x_rows = static_cast<long long>(x_rows);
     p.m = static_cast<int>(m);
     p.G = static_cast<int>(G);

@@ -26,12 +26,21 @@
 
 namespace bqg {
 
+constexpr int kStreamMaxGroup = 512;  // calls per launch (kernel-parameter array, 16 KiB)
+// EVERY fast-path workspace starts with one completion counter per call of a
+// grouped launch (zero between launches: the texture form resets what it
+// uses); every form's partial sums start after them, so forms that share a
+// workspace (a layer handle's, the grouped host pipeline's) never clobber the
+// counters.
+constexpr size_t kTexCounterBytes = kStreamMaxGroup * sizeof(unsigned);
+
 struct QueryParams {
     const uint8_t* keys;    // tiled
     const float* alpha;     // beta x m or nullptr (plane mode: alpha = 1)
     const float* x;         // x_rows x b
     float* y;               // m x b
-    float* partial;         // workspace: plane-major partial sums (layout per form)
+    float* ws;              // workspace base: kTexCounterBytes of completion counters (grouped/texture forms)
+    float* partial;         // = ws + kTexCounterBytes: partial sums (layout per form)
     long long x_rows;
     int m, G, NB, MT, beta, b, cpb;
     int bt;     // fast form: input columns per column tile (1, 2 or 4)
@@ -46,11 +55,6 @@ struct StreamCall {
     const float* x;       // x_rows x 1
     float* y;             // m x 1
 };
-constexpr int kStreamMaxGroup = 512;  // calls per launch (kernel-parameter array, 16 KiB)
-// The grouped workspace starts with one completion counter per call of a
-// launch (zero between launches: the kernel resets what it uses), then the
-// partial sums.
-constexpr size_t kTexCounterBytes = kStreamMaxGroup * sizeof(unsigned);
 bool stream_supported(int mu, int beta, long long b);
 size_t stream_workspace_bytes(long long m, long long groups, int count);
 cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
