@@ -266,13 +266,13 @@ def test_shared_workspace_keeps_the_grouped_counters(bq, port, cuda):
         keys, alpha = L.export()
         ents.append((bq.tile_keys(torch.from_numpy(keys).cuda(), n, mu), torch.from_numpy(alpha).cuda(),
                      torch.from_numpy(x[i]).cuda(), torch.full((m, 1), float("nan"), device="cuda")))
-    for sub in (ents, ents[:2], ents, ents[1:3], ents):
+    for idx in (range(6), range(2), range(6), range(1, 3), range(6)):
+        sub = [ents[i] for i in idx]
         for e in sub:
             e[3].fill_(float("nan"))
         bq.biqgemm_grouped_device(sub, n, m, n, 1, beta, mu, ws)
         torch.cuda.synchronize()
-        for e in sub:
-            i = ents.index(e)
-            assert_close(e[3].cpu().numpy(), refs[i])
+        for i in idx:
+            assert_close(ents[i][3].cpu().numpy(), refs[i])
     for L in layers:
         L.close()
