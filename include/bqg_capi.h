@@ -293,9 +293,13 @@ int bqg_layer_forward_host(bqg_layer* layer, const float* h_x, size_t x_rows, si
  * b) contiguous, h_y is count x (m x b).  H2D of x, the grouped kernels
  * (bqg_biqgemm_grouped_f32) and D2H of y are pipelined in sub-groups sized
  * by host I/O (C2: 64, 128, 256 ... 128, 64 calls) on three streams;
- * synchronised before return.  Runs on a per-device library stream with its own staging and
- * workspace (thread-safe; calls are serialised).  exact != 0: the exact path per
- * layer.  stats (may be NULL) accumulates the counters of all calls. */
+ * synchronised before return.  When the same layers (by identity, not
+ * address), the same pinned h_x / h_y and the same shape recur, the
+ * pipeline is captured on the second occurrence and from then on replayed
+ * as one CUDA graph launch.  Runs on a per-device library stream with its
+ * own staging and workspace (thread-safe; calls are serialised).  exact != 0:
+ * the exact path per layer.  stats (may be NULL) accumulates the counters of
+ * all calls (stats calls are never captured). */
 int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, const float* h_x, size_t x_rows,
                             size_t b, float* h_y, int exact, bqg_kernel_stats* stats);
 /* Device-resident forward on a caller stream (no copies, no sync). */

@@ -276,3 +276,39 @@ def test_shared_workspace_keeps_the_grouped_counters(bq, port, cuda):
             assert_close(ents[i][3].cpu().numpy(), refs[i])
     for L in layers:
         L.close()
+
+
+def test_layers_forward_host_graph_replay(bq, port, cuda):
+    """From the second identical bqg_layers_forward_host call on, a captured
+    graph is replayed: same y as the eager path, bit for bit; new inputs in the same
+    pinned buffers are picked up; a destroyed-and-recreated layer set (new
+    uids) is not confused with the captured one."""
+    import torch
+
+    m, n, beta, mu, count = 256, 512, 2, 8, 9
+    layers = [bq.PackedLinear.from_weights(bq.random_uniform(m, n, 500 + i), beta, mu) for i in range(count)]
+    grp = bq.LayerGroup(layers)
+    x_pin = torch.from_numpy(np.stack([bq.random_normal(n, 1, 600 + i) for i in range(count)])).pin_memory()
+    y_pin = torch.empty((count, m, 1), dtype=torch.float32).pin_memory()
+    outs = []
+    for _ in range(4):  # eager, capture, replay, replay
+        y_pin.fill_(float("nan"))
+        bq.layers_forward_into(grp, x_pin, y_pin)
+        outs.append(y_pin.numpy().copy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    for i, L in enumerate(layers):
+        keys, alpha = L.export()
+        assert_close(outs[0][i], port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x_pin[i].numpy())[0])
+    x_pin.copy_(torch.from_numpy(np.stack([bq.random_normal(n, 1, 700 + i) for i in range(count)])))
+    bq.layers_forward_into(grp, x_pin, y_pin)  # replayed graph reads the buffer's new contents
+    keys, alpha = layers[3].export()
+    assert_close(y_pin[3].numpy(), port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x_pin[3].numpy())[0])
+    for L in layers:
+        L.close()
+    layers2 = [bq.PackedLinear.from_weights(bq.random_uniform(m, n, 800 + i), beta, mu) for i in range(count)]
+    bq.layers_forward_into(bq.LayerGroup(layers2), x_pin, y_pin)
+    keys, alpha = layers2[5].export()
+    assert_close(y_pin[5].numpy(), port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x_pin[5].numpy())[0])
+    for L in layers2:
+        L.close()
