@@ -607,7 +607,11 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
     if (kTexDbg & 1) return;
     move_to(nruns - 1);
     mbar_arrive(&ldone[cur % kNL]);
+#if BQG_TEX_BPOLL
     mbar_wait_poll(fbar, 0, 256);  // the CTA's last tasks are posted: everyone helps finish them
+#else
+    mbar_wait_sleep(fbar, 0);  // the CTA's last tasks are posted: everyone helps finish them
+#endif
     fin_drain(A, fq, tcur, lane);
 }
 
