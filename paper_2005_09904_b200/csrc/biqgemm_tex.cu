@@ -437,14 +437,12 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
     if (sbase + 1024u > lut_abs || lut_abs + 0x10000u > sbase + kTexSmem) __trap();
     uint64_t* lfull = reinterpret_cast<uint64_t*>(smem);  // [kNL] LUT(q) built       (kNBW*32 lanes)
     uint64_t* ldone = lfull + kNL;                        // [kNL] run q gathered      (kNW*32 lanes)
-    uint64_t* fbar = ldone + kNL;  // every run signalled (builder lane 0): the queue is final
     FinQueue* fq = reinterpret_cast<FinQueue*>(smem + 64);
     if (threadIdx.x == 0) {
         for (int b = 0; b < kNL; ++b) {
             mbar_init(&lfull[b], kNBW * 32);
             mbar_init(&ldone[b], kNW * 32);
         }
-        mbar_init(fbar, 1);
         fq->posted = 0;
         fence_mbar_init();
     }
@@ -500,7 +498,12 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
             const int buf = q % kNL;
             // LUT buffer `buf` is free once run q - kNL is gathered; the gather
             // warps are then on run q - 1, which lasts far longer than a poll
-            if (q >= kNL) builder_wait(&ldone[buf], static_cast<uint32_t>((q / kNL - 1) & 1));
+            if (q >= kNL) {
+                // one builder warp polls; the others sleep on a named barrier
+                // (a blocked warp issues nothing: 4x fewer polling slots)
+                if (which == 0) builder_wait(&ldone[buf], static_cast<uint32_t>((q / kNL - 1) & 1));
+                named_bar_sync(2, kNBW * 32);
+            }
 #if !BQG_TEX_BFIRST
             if (q >= kNL) {
                 signal_run(q - kNL);
@@ -522,11 +525,12 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
             }
         }
         for (int q = max(0, nruns - kNL); q < nruns; ++q) {
-            builder_wait(&ldone[q % kNL], static_cast<uint32_t>((q / kNL) & 1));
+            if (which == 0) builder_wait(&ldone[q % kNL], static_cast<uint32_t>((q / kNL) & 1));
             signal_run(q);
         }
         named_bar_sync(1, kNBW * 32);
-        if (which == 0 && lane == 0) mbar_arrive(fbar);  // release: the queue is final
+        // release: the queue is final (the gather warps sleep on barrier 3)
+        if (which == 0) named_bar_arrive(3, (kNW + 1) * 32);
         fin_drain(A, fq, tcur, lane);
         return;
     }
@@ -607,11 +611,7 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
     if (kTexDbg & 1) return;
     move_to(nruns - 1);
     mbar_arrive(&ldone[cur % kNL]);
-#if BQG_TEX_BPOLL
-    mbar_wait_poll(fbar, 0, 256);  // the CTA's last tasks are posted: everyone helps finish them
-#else
-    mbar_wait_sleep(fbar, 0);  // the CTA's last tasks are posted: everyone helps finish them
-#endif
+    named_bar_sync(3, (kNW + 1) * 32);  // the CTA's last tasks are posted: everyone helps finish them
     fin_drain(A, fq, tcur, lane);
 }
 

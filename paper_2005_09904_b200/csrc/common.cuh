@@ -219,6 +219,10 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst_smem, const void* src, 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+// Arrive without waiting (the producer side of a named-barrier handoff).
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // ---- thread-block clusters ---------------------------------------------------
 
