@@ -31,6 +31,10 @@
 #include "kernels.h"
 #include "lut_build.cuh"  // Log2
 
+#ifndef BQG_LAT_PIECE
+#define BQG_LAT_PIECE 8
+#endif
+
 namespace bqg {
 
 // Per-CTA timeline (BQG_DEBUG_FLAGS & 2): globaltimer ns at start, after the
@@ -59,8 +63,9 @@ constexpr int kTable = 1 << kMU;
 constexpr int kLW = 18;                    // warps per CTA (all gather; the first 16 build)
 constexpr int kLB = 16;                    // builder warps
 constexpr int kLThreads = kLW * 32;
-constexpr int kPieceChunks = 8;            // 8 KiB per key copy
-constexpr int kMaxPieces = 32;
+constexpr int kPieceChunks = BQG_LAT_PIECE;  // chunks (KiB) per key copy
+constexpr int kMaxPieces = 64;
+constexpr int kBarBytes = 1024;  // kbar[kMaxPieces] + abar + pbar
 constexpr uint32_t kLutBase = 0x10000u;
 constexpr int kLatSmem = 227 * 1024;
 
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
     uint64_t* kbar = reinterpret_cast<uint64_t*>(smem);   // [kMaxPieces]
     uint64_t* abar = kbar + kMaxPieces;                   // alpha landed
     uint64_t* pbar = abar + 1;                            // pushes into this CTA landed
-    float* as = reinterpret_cast<float*>(smem + 512);      // [BETA][nt*32]
+    float* as = reinterpret_cast<float*>(smem + kBarBytes);  // [BETA][nt*32]
     float* psum = as + BETA * nt * 32;                     // [nchunk][32]
     float* slots = psum + nchunk * 32;                     // [NB][rpo]
     const uint32_t lo_end = smem_u32(slots + A.NB * rpo);
@@ -494,7 +499,7 @@ bool plan_latency(const QueryParams& p, LatArgs& A, int& nclusters) {
     // shared-memory fit of the largest cluster range (keys, alpha, sums, slots)
     {
         const long long nt = A.tq + (A.tr ? 1 : 0);
-        const long long lo = 512 + 4 * nt * 32 * p.beta + 4 * nt * 32 * p.beta * A.bpc +
+        const long long lo = kBarBytes + 4 * nt * 32 * p.beta + 4 * nt * 32 * p.beta * A.bpc +
                              4LL * A.NB * ((nt * 32 + A.CS - 1) / A.CS);
         const long long keys = nt * p.beta * A.bpc * 1024;
         const bool fits = lo + 1024 <= 0x10000 - 1024 && (lo + keys + 1024 <= 0x10000 - 1024 || 0x20000 + keys <= kLatSmem) &&
