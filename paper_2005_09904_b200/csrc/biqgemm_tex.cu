@@ -759,10 +759,12 @@ cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_r
     std::sort(order.begin(), order.end());
     std::vector<int> win_of(count);
     std::vector<std::pair<uintptr_t, uintptr_t>> wins;  // [base, top)
+    static const bool exact_win = getenv("BQG_TEX_EXACTWIN") != nullptr;  // diagnostics
     for (const auto& pr : order) {
-        const uintptr_t lo = pr.first & ~(kWinAlign - 1);
-        const uintptr_t hi = (pr.first + key_bytes + kWinAlign - 1) & ~(kWinAlign - 1);
-        if (!wins.empty() && static_cast<long long>((std::max(hi, wins.back().second) - wins.back().first) / 16) <= texels) {
+        const uintptr_t lo = exact_win ? pr.first : pr.first & ~(kWinAlign - 1);
+        const uintptr_t hi = exact_win ? pr.first + key_bytes : (pr.first + key_bytes + kWinAlign - 1) & ~(kWinAlign - 1);
+        if (!exact_win && !wins.empty() &&
+            static_cast<long long>((std::max(hi, wins.back().second) - wins.back().first) / 16) <= texels) {
             wins.back().second = std::max(hi, wins.back().second);
         } else {
             wins.push_back({lo, hi});

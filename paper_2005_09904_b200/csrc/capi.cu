@@ -812,14 +812,25 @@ int layer_from_device_weights(const float* d_w, size_t m, size_t n, unsigned bet
     return layer_finish_tiling(L);
 }
 
+// Grow a library-owned device buffer.  The zero fill is queued on the stream
+// that will use the buffer: the library's streams are non-blocking, so a
+// legacy-stream cudaMemset is NOT ordered before their kernels and could land
+// in the middle of (or after) the first call that uses the buffer -- seen as
+// a wrong first result when another process shares the GPU.
 template <typename P>
-int grow(P*& ptr, size_t& cap, size_t need) {
+int grow(P*& ptr, size_t& cap, size_t need, cudaStream_t stream) {
     if (need <= cap) return BQG_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    BQG_CUDA(cudaStreamIsCapturing(stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "workspace growth while the stream is being captured: run the "
+                                                 "call once before capturing it");
+    if (ptr) BQG_CUDA(cudaStreamSynchronize(stream));  // queued work may still read the old buffer
     cudaFree(ptr);
     ptr = nullptr;
     cap = 0;
     BQG_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), need));
-    BQG_CUDA(cudaMemset(ptr, 0, need));  // workspaces must start zero-filled (grouped counters)
+    BQG_CUDA(cudaMemsetAsync(ptr, 0, need, stream));  // workspaces start zero-filled (grouped counters)
     cap = need;
     return BQG_OK;
 }
@@ -958,7 +969,7 @@ int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float
     if (exact || L->mu > 8) {
         const size_t need = bqg_biqgemm_exact_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
         if (need > L->ws_exact_bytes) ++L->buf_gen;
-        int s = grow(L->d_ws_exact, L->ws_exact_bytes, need);
+        int s = grow(L->d_ws_exact, L->ws_exact_bytes, need, st);
         if (s) return s;
         return biqgemm_exact_impl<float>(L->d_keys, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu,
                                          exact == BQG_FORWARD_EXACT_NAIVE ? BQG_LUT_NAIVE : BQG_LUT_DP,
@@ -967,7 +978,7 @@ int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float
     const size_t need = bqg_biqgemm_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
     if (need > L->ws_bytes) {
         ++L->buf_gen;
-        int s = grow(L->d_ws, L->ws_bytes, need);
+        int s = grow(L->d_ws, L->ws_bytes, need, st);
         if (s) return s;
     }
     return bqg_biqgemm_f32(L->d_tiled, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu, L->d_ws,
@@ -1014,9 +1025,9 @@ extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_r
     std::lock_guard<std::mutex> g(L->mu_lock);
     const size_t xbytes = sizeof(float) * x_rows * b, ybytes = sizeof(float) * L->m * b;
     if (xbytes > L->x_cap || ybytes > L->y_cap || xbytes > L->hx_cap || ybytes > L->hy_cap) ++L->buf_gen;
-    s = grow(L->d_x, L->x_cap, xbytes);
+    s = grow(L->d_x, L->x_cap, xbytes, L->stream);
     if (s) return s;
-    s = grow(L->d_y, L->y_cap, ybytes);
+    s = grow(L->d_y, L->y_cap, ybytes, L->stream);
     if (s) return s;
     // Steady state (no stats requested): the caller's x is copied into the
     // layer's pinned staging, one cached CUDA graph runs H2D -> kernels ->
@@ -1200,9 +1211,9 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
         BQG_CUDA(cudaEventCreateWithFlags(&G.join_dp, cudaEventDisableTiming));
     }
     const size_t xs = x_rows * b, ys = L0->m * b;
-    s = grow(G.d_x, G.x_cap, sizeof(float) * xs * count);
+    s = grow(G.d_x, G.x_cap, sizeof(float) * xs * count, G.stream);
     if (s) return s;
-    s = grow(G.d_y, G.y_cap, sizeof(float) * ys * count);
+    s = grow(G.d_y, G.y_cap, sizeof(float) * ys * count, G.stream);
     if (s) return s;
     // Pipelined in sub-groups: the H2D of sub-group k+1 (copy stream) and the
     // D2H of sub-group k-1 (down stream) overlap the kernels of sub-group k
@@ -1271,7 +1282,7 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
         G.chunk_ev.push_back(e);
     }
     s = grow(G.d_ws, G.ws_cap,
-             bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, std::min(count, kSub)));
+             bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, std::min(count, kSub)), G.stream);
     if (s) return s;
     std::vector<bqg_call> calls(count);
     for (size_t i = 0; i < count; ++i) calls[i] = {layers[i]->d_tiled, layers[i]->d_alpha, G.d_x + i * xs, G.d_y + i * ys};
