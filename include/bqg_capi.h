@@ -302,7 +302,9 @@ int bqg_layer_forward_host(bqg_layer* layer, const float* h_x, size_t x_rows, si
  * all calls (stats calls are never captured). */
 int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, const float* h_x, size_t x_rows,
                             size_t b, float* h_y, int exact, bqg_kernel_stats* stats);
-/* Device-resident forward on a caller stream (no copies, no sync). */
+/* Device-resident forward on a caller stream (no copies, no sync).  The
+ * layer's workspace is shared by its calls: calls on DIFFERENT streams must
+ * not overlap in time (order them, or give each stream its own layer). */
 int bqg_layer_forward_device(bqg_layer* layer, const float* d_x, size_t x_rows, size_t b, float* d_y,
                              int exact, int pdl, void* stream);
 

@@ -231,10 +231,13 @@ def build_lut_block(x, group_begin: int, group_count: int, mu: int, layout: int 
 
 
 class Workspace:
-    """Zero-initialised fast-path workspace (the kernel leaves it zeroed)."""
+    """Zero-initialised fast-path workspace (the kernel leaves it zeroed).
+    The fill is complete before the constructor returns: the library's
+    launches may run on any (non-blocking) stream."""
 
     def __init__(self, nbytes: int, device="cuda"):
         self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        torch.cuda.synchronize(self.buf.device)
 
     @property
     def nbytes(self):
