@@ -15,7 +15,7 @@ __device__ __forceinline__ unsigned long long gt() {
     return t;
 }
 
-__global__ void burst(const unsigned char* src, size_t per_cta, int pieces, unsigned long long* out) {
+__global__ void burst(const unsigned char* src, size_t per_cta, int pieces, unsigned long long* out, int spin) {
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
     unsigned char* dst = sm + 1024;
@@ -29,14 +29,31 @@ __global__ void burst(const unsigned char* src, size_t per_cta, int pieces, unsi
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int p = lane; p < pieces; p += 32) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[p])), "r"(piece) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             smem_u32(dst + p * piece)),
-                         "l"(src + blockIdx.x * per_cta + p * piece), "r"(piece), "r"(smem_u32(&bar[p]))
-                         : "memory");
+            if (spin & 4) {
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                                 smem_u32(dst + p * piece)),
+                             "l"(src + blockIdx.x * per_cta + p * piece), "r"(piece), "r"(smem_u32(&bar[p])), "l"(pol)
+                             : "memory");
+            } else {
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_u32(dst + p * piece)),
+                             "l"(src + blockIdx.x * per_cta + p * piece), "r"(piece), "r"(smem_u32(&bar[p]))
+                             : "memory");
+            }
         }
     }
     const unsigned long long t1 = gt();
+    if (spin & 2) asm volatile("griddepcontrol.launch_dependents;" :::);
+    if (spin & 2) asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
+    if ((spin & 1) && warp > 0) {  // the latency form's gather warps: spin on the pieces meanwhile
+        const int p = (warp - 1) % pieces;
+        asm volatile("{\n\t.reg .pred q;\nS_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t@!q bra S_%=;\n}" ::"r"(
+                         smem_u32(&bar[p]))
+                     : "memory");
+    }
     if (threadIdx.x == 0) {
         for (int p = 0; p < pieces; ++p)
             asm volatile("{\n\t.reg .pred q;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%0], 0;\n\t@!q bra W_%=;\n}" ::"r"(
@@ -59,9 +76,12 @@ int main() {
     cudaMalloc(&out, 148 * 3 * 8);
     cudaFuncSetAttribute(burst, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(burst, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    struct V { int grid, cs, smem_kb, pieces, threads; };
-    std::vector<V> vs = {{120, 1, 227, 7, 576}, {120, 8, 227, 7, 576}, {148, 1, 227, 7, 576}, {120, 8, 64, 7, 576},
-                         {120, 1, 64, 7, 576}, {120, 8, 227, 28, 576}, {120, 1, 227, 28, 576}, {120, 8, 227, 7, 128}};
+    struct V { int grid, cs, smem_kb, pieces, threads, spin; };
+    std::vector<V> vs = {{120, 1, 227, 7, 576, 0}, {120, 8, 227, 7, 576, 0}, {148, 1, 227, 7, 576, 0},
+                         {120, 8, 64, 7, 576, 0},  {120, 1, 64, 7, 576, 0},  {120, 8, 227, 28, 576, 0},
+                         {120, 1, 227, 28, 576, 0}, {120, 8, 227, 7, 128, 0}, {120, 8, 227, 7, 576, 1},
+                         {120, 1, 227, 7, 576, 1}, {120, 8, 227, 7, 576, 2}, {120, 8, 227, 7, 576, 3},
+                         {120, 8, 227, 7, 576, 4}, {120, 8, 227, 7, 576, 6}};
     for (auto v : vs) {
         std::vector<double> issued, landed;
         for (int rep = 0; rep < 30; ++rep) {
@@ -69,15 +89,22 @@ int main() {
             cfg.gridDim = dim3(v.grid);
             cfg.blockDim = dim3(v.threads);
             cfg.dynamicSmemBytes = v.smem_kb * 1024;
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = v.cs;
             at[0].val.clusterDim.y = 1;
             at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[1].val.programmaticStreamSerializationAllowed = (v.spin & 2) ? 1 : 0;
             cfg.attrs = at;
-            cfg.numAttrs = 1;
+            cfg.numAttrs = 2;
             const unsigned char* s = src + (rep % copies) * per_cta * 148;
-            cudaLaunchKernelEx(&cfg, burst, s, per_cta, v.pieces, out);
+            if (v.spin & 2) {  // a PDL chain of 20 launches; the last one is recorded
+                for (int k = 0; k < 20; ++k)
+                    cudaLaunchKernelEx(&cfg, burst, src + ((rep * 20 + k) % copies) * per_cta * 148, per_cta, v.pieces, out, v.spin);
+            } else {
+                cudaLaunchKernelEx(&cfg, burst, s, per_cta, v.pieces, out, v.spin);
+            }
             cudaDeviceSynchronize();
             if (rep < 10) continue;
             std::vector<unsigned long long> h(148 * 3);
@@ -91,8 +118,8 @@ int main() {
         }
         std::sort(issued.begin(), issued.end());
         std::sort(landed.begin(), landed.end());
-        printf("grid %3d cluster %d smem %3d KB pieces %2d threads %3d: issued med %.2f  landed med %.2f max %.2f us  (%.1f GB/s/SM)\n",
-               v.grid, v.cs, v.smem_kb, v.pieces, v.threads, issued[issued.size() / 2], landed[landed.size() / 2],
+        printf("spin %d grid %3d cluster %d smem %3d KB pieces %2d threads %3d: issued med %.2f  landed med %.2f max %.2f us  (%.1f GB/s/SM)\n",
+               v.spin, v.grid, v.cs, v.smem_kb, v.pieces, v.threads, issued[issued.size() / 2], landed[landed.size() / 2],
                landed.back(), per_cta / (landed[landed.size() / 2] * 1e3));
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
