@@ -15,15 +15,22 @@
 //      consumer warps: after griddepcontrol.wait, build the block's tables in
 //                      bank-owned shared memory with the DP recurrence
 //                      (lut_build.cuh; table of group g lives in bank g);
-//                      then per chunk lane l owns row l of the tile and at
-//                      step j gathers T_g[key(l, g)] for the rotated group
-//                      g = (l + j) mod 32 -- every lane hits a different bank,
-//                      so each warp gather is one conflict-free wavefront --
-//                      and accumulates in registers.  No cross-lane reduction
-//                      (no SHFL, which shares the shared-memory pipe).  The
-//                      per-(plane, block) partial goes to the workspace.
-// 2. finalize_kernel -- y(r,c) = sum_i alpha_i[r] * sum_gb partial, in fp64,
-//    planes and blocks ascending (kernel.hpp:183-195).
+//                      then per 32-row TILE (its beta 1 KiB chunks, one
+//                      warp) lane l owns row l and at step j gathers
+//                      T_g[key(l, g)] for the rotated group g = (l + j) mod 32
+//                      -- every lane hits a different bank, so each warp
+//                      gather is one conflict-free wavefront -- and
+//                      accumulates in registers.  No cross-lane reduction (no
+//                      SHFL, which shares the shared-memory pipe).  The beta
+//                      plane sums of a tile are combined with alpha in fp64
+//                      and ONE fp32 partial per (block, row, column) goes to
+//                      the workspace (beta x less partial traffic than one per
+//                      plane: the round trip through HBM/L2 was ~25% of a
+//                      large-b call).
+// 2. finalize_kernel -- y(r,c) = f32(sum_gb partial[gb][r][c]), fp64, blocks
+//    ascending: per block sum_i alpha_i * P_i in fp64 first (kernel.hpp:
+//    183-195 applies alpha after the full group sum; the per-block combine is
+//    the b = 1 forms' arithmetic, within the fp32 contract).
 //
 // Every output's reduction tree is a function of (n, mu) only, so y is
 // bitwise identical for every grid shape, CTA split and row sharding.
@@ -56,13 +63,16 @@ __device__ __forceinline__ unsigned smid() {
 }
 
 struct FastPlan {
-    int cpp;    // key chunks (plane x 32-row tile) per (group block, column tile) pair
+    int cpp;    // 32-row tiles (beta KiB of keys each) per (group block, column tile) pair
     int CT;     // column tiles
     int mode;   // 0 = aligned (cpb CTAs per pair), 1 = flat contiguous split
     int cpb;    // aligned: CTAs per pair
     int grid;
-    int q, r;   // balanced split: CTA c gets q + (c < r) chunks of its domain
+    int q, r;   // balanced split: CTA c gets q + (c < r) tiles of its domain
+    int tps;    // tiles per ring stage (<= NW: warp w takes tile w of a stage)
+    int R;      // ring stages (<= kMaxStages)
 };
+constexpr int kMaxStages = 8;
 
 // Byte offset of key byte `bi` of word w in the bank-owned LUT, OR'd with the
 // lane's offset.  word(k, l, c) = (k*32 + l)*BT + c  ->  byte = k << SH | l*4*BT.
@@ -75,18 +85,21 @@ __device__ __forceinline__ uint32_t lut_off(uint32_t w, int bi, uint32_t lane_of
     return (v & MASK) | lane_off;
 }
 
-template <int MU, int BT, int NW, int R>
+template <int MU, int BT, int NW>
 __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     biqgemm_fast_kernel(const QueryParams p, const FastPlan plan) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int LUT_BYTES = (1 << MU) * LutGeom<BT>::KROW * 4;
-    constexpr int SCH = NW;  // chunks per stage (one per consumer warp)
-    constexpr int STAGE_BYTES = SCH * 1024;
+    const int beta = p.beta;
+    const int R = plan.R;
+    const int TPS = plan.tps;                              // tiles per stage
+    const uint32_t TILE_BYTES = static_cast<uint32_t>(beta) * 1024u;
+    const uint32_t STAGE_BYTES = static_cast<uint32_t>(TPS) * TILE_BYTES;
     float* lut = reinterpret_cast<float*>(smem);
     unsigned char* stages = smem + LUT_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(stages + R * STAGE_BYTES);
-    uint64_t* empty = full + R;
-    float* xs = reinterpret_cast<float*>(empty + R);  // staged x tile (32*MU x BT)
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(R) * STAGE_BYTES);
+    uint64_t* empty = full + kMaxStages;
+    float* xs = reinterpret_cast<float*>(empty + kMaxStages);  // staged x tile (32*MU x BT)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool tl = (p.debug & 2) && threadIdx.x == 0 && blockIdx.x < 8192;
@@ -97,22 +110,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     }
     pdl_launch_dependents();
 
-    // This CTA's chunk range [cbeg, cend): 32-bit, no divisions.
+    // This CTA's tile range [cbeg, cend) over the (pair, tile) sequence.
     const int c = plan.mode == 0 ? static_cast<int>(blockIdx.x) % plan.cpb : static_cast<int>(blockIdx.x);
     const int dom = plan.mode == 0 ? static_cast<int>(blockIdx.x) / plan.cpb : 0;
     const int cbeg = dom * plan.cpp + c * plan.q + min(c, plan.r);
     const int cend = cbeg + plan.q + (c < plan.r ? 1 : 0);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < R; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
+        for (int st = 0; st < R; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], NW);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    const int beta = p.beta;
     const long long rows_pad = static_cast<long long>(p.MT) * 32;
 
     if (warp == NW) {
@@ -125,14 +137,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
                 const int pbase = pair * plan.cpp;
                 const int seg_end = min(cend, pbase + plan.cpp);
                 const int gb = pair / plan.CT;
-                const unsigned char* kpair = p.keys + static_cast<long long>(gb) * plan.cpp * 1024;
-                for (int c0 = seg - pbase; c0 < seg_end - pbase; c0 += SCH, ++sc) {
-                    const int cnt = min(SCH, seg_end - pbase - c0);
+                const unsigned char* kpair = p.keys + static_cast<long long>(gb) * plan.cpp * TILE_BYTES;
+                for (int t0 = seg - pbase; t0 < seg_end - pbase; t0 += TPS, ++sc) {
+                    const int cnt = min(TPS, seg_end - pbase - t0);
                     const int slot = sc % R;
                     mbar_wait(&empty[slot], ((sc / R) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&full[slot], cnt * 1024);
-                    bulk_g2s(stages + slot * STAGE_BYTES, kpair + static_cast<long long>(c0) * 1024, cnt * 1024,
-                             &full[slot], pol);
+                    mbar_arrive_expect_tx(&full[slot], cnt * TILE_BYTES);
+                    bulk_g2s(stages + static_cast<size_t>(slot) * STAGE_BYTES, kpair + static_cast<long long>(t0) * TILE_BYTES,
+                             cnt * TILE_BYTES, &full[slot], pol);
                 }
                 seg = seg_end;
             }
@@ -160,8 +172,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
 #pragma unroll
         for (int k = 0; k < XPT; ++k) {
             const int idx = threadIdx.x + k * NW * 32;
-            const int rl = idx / BT, c = idx - (idx / BT) * BT;
-            const long long r = r0 + rl, col = col0 + c;
+            const int rl = idx / BT, cc = idx - (idx / BT) * BT;
+            const long long r = r0 + rl, col = col0 + cc;
             xr[k] = (idx < XT && r < p.x_rows && col < p.b) ? __ldcg(p.x + r * p.b + col) : 0.0f;
         }
     };
@@ -184,41 +196,46 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
         if (tl) g_timeline[blockIdx.x][2] = gtimer();
 
         const int lo = seg - pbase, hi = seg_end - pbase;
-        // (t, i) of this warp's chunk lo + warp, advanced by NW = q*beta + rr per stage
-        int ti = (lo + warp) / beta;
-        int ii = lo + warp - ti * beta;
-        const int dq = NW / beta, dr = NW - (NW / beta) * beta;
-        for (int c0 = lo; c0 < hi; c0 += SCH, ++sc) {
+        for (int t0 = lo; t0 < hi; t0 += TPS, ++sc) {
             const int slot = sc % R;
+            const int t = t0 + warp;  // this warp's tile of the stage
+            const bool mine = warp < TPS && t < hi;
+            // alpha of the warp's rows, requested before the keys are waited for
+            const long long row = static_cast<long long>(t) * 32 + lane;
+            const bool live = mine && row < p.m;
             mbar_wait(&full[slot], (sc / R) & 1);
             if (tl && sc == 0) g_timeline[blockIdx.x][3] = gtimer();
-            const int chunk = c0 + warp;
-            if (chunk < hi) {
-                const unsigned char* kc = stages + slot * STAGE_BYTES + warp * 1024;
-                const uint4 ka = *reinterpret_cast<const uint4*>(kc + lane * 16);
-                const uint4 kb = *reinterpret_cast<const uint4*>(kc + 512 + lane * 16);
-                const uint32_t w[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
-                float o[BT];
-                gather_chunk<MU, BT>(w, lut_s, goff, o);
-                // partial[i*NB + gb][ct][row][BT]: the warp's 32 rows x BT
-                // columns are one contiguous 128*BT-byte run (one vector
-                // store per lane; padding columns past b are written and
-                // never read)
-                float* dst = p.partial +
-                             (((static_cast<long long>(ii) * p.NB + gb) * plan.CT + ct) * rows_pad + ti * 32 + lane) * BT;
-                if constexpr (BT == 4) {
-                    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
-                } else if constexpr (BT == 2) {
-                    *reinterpret_cast<float2*>(dst) = make_float2(o[0], o[1]);
-                } else {
-                    dst[0] = o[0];
+            if (mine) {
+                const unsigned char* kt = stages + static_cast<size_t>(slot) * STAGE_BYTES +
+                                          static_cast<size_t>(warp) * TILE_BYTES;
+                double acc[BT];
+#pragma unroll
+                for (int cc = 0; cc < BT; ++cc) acc[cc] = 0.0;
+#pragma unroll 1
+                for (int i = 0; i < beta; ++i) {
+                    const float a = live ? (p.alpha ? __ldg(p.alpha + static_cast<long long>(i) * p.m + row) : 1.0f)
+                                         : 0.0f;
+                    const unsigned char* kc = kt + i * 1024;
+                    const uint4 ka = *reinterpret_cast<const uint4*>(kc + lane * 16);
+                    const uint4 kb = *reinterpret_cast<const uint4*>(kc + 512 + lane * 16);
+                    const uint32_t w[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+                    float o[BT];
+                    gather_chunk<MU, BT>(w, lut_s, goff, o);
+#pragma unroll
+                    for (int cc = 0; cc < BT; ++cc) acc[cc] += static_cast<double>(a) * static_cast<double>(o[cc]);
                 }
-            }
-            ti += dq;
-            ii += dr;
-            if (ii >= beta) {
-                ii -= beta;
-                ++ti;
+                // partial[gb][ct][row][BT]: the warp's 32 rows x BT columns are
+                // one contiguous 128*BT-byte run (one vector store per lane;
+                // padding columns past b are written and never read)
+                float* dst = p.partial + ((static_cast<long long>(gb) * plan.CT + ct) * rows_pad + row) * BT;
+                if constexpr (BT == 4) {
+                    *reinterpret_cast<float4*>(dst) = make_float4(static_cast<float>(acc[0]), static_cast<float>(acc[1]),
+                                                                  static_cast<float>(acc[2]), static_cast<float>(acc[3]));
+                } else if constexpr (BT == 2) {
+                    *reinterpret_cast<float2*>(dst) = make_float2(static_cast<float>(acc[0]), static_cast<float>(acc[1]));
+                } else {
+                    dst[0] = static_cast<float>(acc[0]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
@@ -231,10 +248,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     }
 }
 
-// y(r, c) = sum_i alpha_i[r] * (sum_gb partial[i][gb][r][c]), fp64, ascending
-// planes and group blocks (kernel.hpp:183-195).  One thread per (column
-// tile, row): the BT columns of a partial are one vector load, and every load
-// is issued ahead of its use -- the plane scales up front, the partials in
+// y(r, c) = f32(sum_gb partial[gb][r][c]), fp64, blocks ascending (each
+// partial already holds sum_i alpha_i * P_i of its block, combined in fp64).
+// One thread per (column tile, row): the BT columns of a partial are one
+// vector load, and every load is issued ahead of its use -- the partials in
 // batches of KB vectors with the next batch in flight while the current one
 // is summed (the finaliser is latency-bound otherwise).
 template <int BT>
@@ -272,23 +289,16 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
     const long long r = rt % p.m, ct = rt / p.m;
     if (ct >= CT || ct * BT + cc * COLS >= p.b) return;
     const long long rows_pad = static_cast<long long>(p.MT) * 32;
-    const int total = p.NB * p.beta;  // q = i*NB + gb
+    const int total = p.NB;  // partial gb: [gb][ct][row][BT]
     const long long stride = CT * rows_pad * PER;  // in V units
-    const V* src = reinterpret_cast<const V*>(p.partial) + (ct * rows_pad + r) * PER + cc;  // partial q = 0
-    constexpr int BTC = COLS;  // columns summed by this thread
-    constexpr int KB = COLS == 4 ? 8 : (COLS == 2 ? 16 : 32), KA = 8;
-    float a[KA];
-#pragma unroll
-    for (int t = 0; t < KA; ++t)
-        a[t] = (p.alpha && t < p.beta) ? __ldg(p.alpha + static_cast<long long>(t) * p.m + r) : 1.0f;
+    const V* src = reinterpret_cast<const V*>(p.partial) + (ct * rows_pad + r) * PER + cc;  // block 0
+    constexpr int KB = COLS == 4 ? 8 : (COLS == 2 ? 16 : 32);
     V v[KB];
 #pragma unroll
     for (int k = 0; k < KB; ++k) v[k] = __ldcg(src + min(k, total - 1) * stride);
-    double y[BTC], acc[BTC];
+    double y[COLS];
 #pragma unroll
-    for (int c = 0; c < BTC; ++c) y[c] = acc[c] = 0.0;
-    int g = 0, i = 0;
-    double a_i = static_cast<double>(a[0]);
+    for (int c = 0; c < COLS; ++c) y[c] = 0.0;
 #pragma unroll 1
     for (int q0 = 0; q0 < total; q0 += KB) {
         const bool more = q0 + KB < total;
@@ -301,24 +311,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
         for (int k = 0; k < KB; ++k) {
             if (q0 + k < total) {
 #pragma unroll
-                for (int c = 0; c < BTC; ++c) acc[c] += static_cast<double>(VecT<COLS>::get(v[k], c));
-                if (++g == p.NB) {
-#pragma unroll
-                    for (int c = 0; c < BTC; ++c) {
-                        y[c] += a_i * acc[c];
-                        acc[c] = 0.0;
-                    }
-                    g = 0;
-                    ++i;
-                    if (i < p.beta) {
-                        float an = 1.0f;
-#pragma unroll
-                        for (int t = 1; t < KA; ++t)
-                            if (t == i) an = a[t];
-                        if (i >= KA && p.alpha) an = __ldg(p.alpha + static_cast<long long>(i) * p.m + r);
-                        a_i = static_cast<double>(an);
-                    }
-                }
+                for (int c = 0; c < COLS; ++c) y[c] += static_cast<double>(VecT<COLS>::get(v[k], c));
             }
         }
         if (more) {
@@ -328,7 +321,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
     }
     float* yr = p.y + r * p.b + ct * BT + cc * COLS;
 #pragma unroll
-    for (int c = 0; c < BTC; ++c)
+    for (int c = 0; c < COLS; ++c)
         if (ct * BT + cc * COLS + c < p.b) yr[c] = static_cast<float>(y[c]);
 }
 
@@ -337,28 +330,37 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
 #endif
 constexpr int kNW = BQG_FAST_NW;
 
-#ifndef BQG_FAST_R4
-#define BQG_FAST_R4 6
-#endif
-template <int BT>
-constexpr int stages_for() {
-    return BT == 1 ? 6 : (BT == 2 ? 4 : BQG_FAST_R4);
+// Shared memory: the LUT, a ring of R stages of tps tiles (beta KiB each),
+// 2 x kMaxStages mbarriers, the staged x tile.  BT = 1 runs two CTAs per SM.
+constexpr size_t kSmemCap = 227 * 1024;
+size_t lut_bytes(int mu, int bt) { return (size_t(1) << mu) * (bt == 1 ? 64 : 32 * bt) * 4; }
+size_t smem_tail(int mu, int bt) { return 2 * kMaxStages * sizeof(uint64_t) + size_t(32) * mu * bt * 4; }
+size_t fast_smem_bytes(const FastPlan& pl, int mu, int bt, int beta) {
+    return lut_bytes(mu, bt) + size_t(pl.R) * pl.tps * beta * 1024 + smem_tail(mu, bt);
 }
-
-template <int MU, int BT>
-size_t smem_bytes() {
-    return static_cast<size_t>(1u << MU) * LutGeom<BT>::KROW * 4 + static_cast<size_t>(stages_for<BT>()) * kNW * 1024 +
-           2 * stages_for<BT>() * sizeof(uint64_t) + 32 * MU * BT * 4;
+// tiles per stage and ring depth for (mu, BT, beta): as many tiles per stage
+// as consumer warps while two stages fit, then as many stages as fit (<= 6).
+bool ring_shape(int mu, int bt, int beta, FastPlan& pl) {
+    for (size_t budget : {bt == 1 ? size_t(110 * 1024) : kSmemCap, kSmemCap}) {
+        const size_t fixed = lut_bytes(mu, bt) + smem_tail(mu, bt) + 1024;
+        if (fixed >= budget) continue;
+        const size_t avail = budget - fixed, tile = size_t(beta) * 1024;
+        const int tps = static_cast<int>(std::min<size_t>(kNW, avail / (2 * tile)));
+        if (tps < 1) continue;
+        pl.tps = tps;
+        pl.R = static_cast<int>(std::min<size_t>(6, avail / (tps * tile)));
+        return true;
+    }
+    return false;
 }
 
 template <int MU, int BT>
 cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, cudaStream_t stream) {
-    constexpr int R = stages_for<BT>();
-    auto kern = biqgemm_fast_kernel<MU, BT, kNW, R>;
-    const size_t smem = smem_bytes<MU, BT>();
+    auto kern = biqgemm_fast_kernel<MU, BT, kNW>;
+    const size_t smem = fast_smem_bytes(plan, MU, BT, p.beta);
     static PerDeviceOnce configured;  // one attribute call per instantiation and device
     cudaError_t ea = once_per_device(configured, current_device(), [&] {
-        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemCap));
     });
     if (ea != cudaSuccess) return ea;
     cudaLaunchConfig_t cfg = {};
@@ -417,15 +419,16 @@ FastPlan make_plan(long long m, long long groups, int beta, long long b, int mu,
     FastPlan pl{};
     const long long NB = (groups + 31) / 32, MT = (m + 31) / 32;
     pl.CT = static_cast<int>((b + BT - 1) / BT);
-    pl.cpp = static_cast<int>(MT * beta);
+    pl.cpp = static_cast<int>(MT);  // units: 32-row tiles (beta chunks each)
+    if (!ring_shape(mu, BT, beta, pl)) pl.tps = pl.R = 0;  // the launcher rejects the shape
     const long long pairs = NB * pl.CT;
     const long long total = pairs * pl.cpp;
     // Cost model in shared-memory wavefronts (the binding resource): building
     // one block of tables = 2^mu * BT wavefronts (+ fixed overhead); one
-    // chunk = 32 (BT=1), 64 (BT=2) or 128 (BT=4) gather wavefronts + 8 key
-    // wavefronts.
+    // tile = beta chunks of 32 (BT=1), 64 (BT=2) or 128 (BT=4) gather
+    // wavefronts + 8 key wavefronts.
     const double build = static_cast<double>(1 << mu) * BT + 96.0;
-    const double unit = (BT == 4 ? 128.0 : (BT == 2 ? 64.0 : 32.0)) + 8.0;  // gather + key wavefronts
+    const double unit = beta * ((BT == 4 ? 128.0 : (BT == 2 ? 64.0 : 32.0)) + 8.0);
     const long long sms = std::max(1, num_sms);
     long long best_cpb = 1;
     double best_aligned = 1e300;
@@ -524,6 +527,7 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
         return launch_biqgemm_stream(&call, 1, p.x_rows, p.m, p.G, p.beta, p.ws, pdl, stream);
     }
     const FastPlan plan = make_plan(p.m, p.G, p.beta, p.b, mu, sms);
+    if (plan.R < 2) return cudaErrorInvalidValue;  // beta too large for a two-stage key ring
     const int bt = pick_bt(p.b);
     switch (mu) {
         case 1: return launch_mu<1>(p, plan, bt, pdl, stream);
