@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
 }
 
 #ifndef BQG_FAST_NW
-#define BQG_FAST_NW 8
+#define BQG_FAST_NW 12
 #endif
 constexpr int kNW = BQG_FAST_NW;
 
