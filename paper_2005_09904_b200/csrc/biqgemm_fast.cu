@@ -333,6 +333,10 @@ constexpr int kNW = BQG_FAST_NW;
 // Shared memory: the LUT, a ring of R stages of tps tiles (beta KiB each),
 // 2 x kMaxStages mbarriers, the staged x tile.  BT = 1 runs two CTAs per SM.
 constexpr size_t kSmemCap = 227 * 1024;
+#ifndef BQG_FAST_MINR
+#define BQG_FAST_MINR 2
+#endif
+constexpr size_t kMinStages = BQG_FAST_MINR;  // ring depth the stage size is chosen for
 size_t lut_bytes(int mu, int bt) { return (size_t(1) << mu) * (bt == 1 ? 64 : 32 * bt) * 4; }
 size_t smem_tail(int mu, int bt) { return 2 * kMaxStages * sizeof(uint64_t) + size_t(32) * mu * bt * 4; }
 size_t fast_smem_bytes(const FastPlan& pl, int mu, int bt, int beta) {
@@ -345,7 +349,7 @@ bool ring_shape(int mu, int bt, int beta, FastPlan& pl) {
         const size_t fixed = lut_bytes(mu, bt) + smem_tail(mu, bt) + 1024;
         if (fixed >= budget) continue;
         const size_t avail = budget - fixed, tile = size_t(beta) * 1024;
-        const int tps = static_cast<int>(std::min<size_t>(kNW, avail / (2 * tile)));
+        const int tps = static_cast<int>(std::min<size_t>(kNW, avail / (kMinStages * tile)));
         if (tps < 1) continue;
         pl.tps = tps;
         pl.R = static_cast<int>(std::min<size_t>(6, avail / (tps * tile)));
