@@ -342,9 +342,18 @@ def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
     x_h = [bq.random_normal(n, b, SEED + 1 + j) for j in range(NX)]
     x_step = torch.from_numpy(np.stack([x_h[i % NX] for i in range(G)])).to(dev)  # [G, n, 1]
     R = m  # rows per rank (m is 32-aligned)
-    y_gather = torch.empty((world, G, R, b), device=dev)
+    peer = None
+    if world > 1:
+        # every rank's gather buffer mapped into every rank (CUDA IPC): the
+        # grouped kernel's finaliser stores y rows straight into all of them
+        from paper_2005_09904_b200.sharded import PeerGather
+
+        peer = PeerGather((world, G, R, b), rank, world, device=dev)
+        y_gather = peer.tensor
+    else:
+        y_gather = torch.empty((world, G, R, b), device=dev)
     y_mine = y_gather[rank]
-    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_workspace_bytes(world * m, n, b, beta, mu, G, world))
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(world * m, n, b, beta, mu, G, world))
                       if world > 1 else int(bq.lib.bqg_biqgemm_grouped_workspace_bytes(m, n, b, beta, mu, G)),
                       device=dev)
 
@@ -369,16 +378,18 @@ def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
 
     coll = ctx.collectives() if world > 1 else None
     if hasattr(coll, "register"):
-        coll.register(x_step, y_gather)
+        coll.register(x_step, y_gather, ws.buf)
     coll_struct = coll.collectives() if coll is not None else None
 
     def sharded_launch(s, pdl=True):
-        """One step at N > 1: broadcast x -> grouped kernel -> all-gather y (C ABI)."""
+        """One step at N > 1 (C ABI): broadcast x -> the grouped kernel on this
+        rank's rows, its finaliser storing y rows into every rank's gather
+        buffer (fused all-gather over peer memory) -> a 16-byte barrier."""
         import ctypes as C
 
-        bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
-            C.cast(shard_arrays[s], C.c_void_p), G, x_step.data_ptr(), n, y_gather.data_ptr(), world * m, n, b, beta,
-            mu, rank, world, C.byref(coll_struct), ws.ptr(), ws.nbytes, 1 if pdl else 0, stream.cuda_stream))
+        bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
+            C.cast(shard_arrays[s], C.c_void_p), G, x_step.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p), world * m, n,
+            b, beta, mu, rank, world, C.byref(coll_struct), ws.ptr(), ws.nbytes, 1 if pdl else 0, stream.cuda_stream))
 
     # ---- correctness gate before timing
     with torch.cuda.stream(stream):
@@ -458,8 +469,9 @@ def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
             f" per rank (layer {world * m}x{n} row-sharded over {world} GPUs)" if world > 1 else ""),
                    "m": m, "n": n, "beta": beta, "mu": mu, "batch": b,
                    "step": f"one grouped launch of {G} independent BiQGEMM calls (own weight copy, own x, own LUT "
-                           f"build, own y each)" + ("; NCCL broadcast of the x batch + all-gather of the y batch "
-                                                    "inside the step (bqg_biqgemm_grouped_sharded_f32)"
+                           f"build, own y each)" + ("; NCCL broadcast of the x batch, the y rows stored by the kernel "
+                                                    "into every rank's IPC-mapped gather buffer (fused all-gather), "
+                                                    "a 16-byte barrier (bqg_biqgemm_grouped_sharded_p2p_f32)"
                                                     if world > 1 else ""),
                    "l2": f"inputs larger than L2: every call reads a different one of {copies} rotating weight "
                          f"copies ({copies * tiled[0].numel() / 1e6:.0f} MB > 4x126 MB L2) at any --steps",
@@ -607,11 +619,14 @@ def e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K):
         al0 = torch.from_numpy(alpha).to(dev)
         n_copies = max(2, int(np.ceil(ROTATE_L2 * L2_BYTES / tiled0.numel())) + 1)
         tl = [tiled0] + [tiled0.clone() for _ in range(n_copies - 1)]
+        from paper_2005_09904_b200.sharded import PeerGather
+
         x_dev = torch.empty((G, n, b), device=dev)
-        y_gather = torch.empty((world, G, m, b), device=dev)
+        peer = PeerGather((world, G, m, b), ctx.rank, world, device=dev)
+        y_gather = peer.tensor
         y_host = torch.empty((world, G, m, b), dtype=torch.float32).pin_memory()
-        ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_workspace_bytes(world * m, n, b, beta, mu, G, world)),
-                          device=dev)
+        ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(world * m, n, b, beta, mu, G,
+                                                                                     world)), device=dev)
         coll = ctx.collectives()
 
         arrays = []
@@ -621,15 +636,15 @@ def e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K):
                 arr[i] = bq._capi.ShardCall(tl[(s * G + i) % n_copies].data_ptr(), al0.data_ptr())
             arrays.append(arr)
         if hasattr(coll, "register"):
-            coll.register(x_dev, y_gather)
+            coll.register(x_dev, y_gather, ws.buf)
         cs = coll.collectives()
 
         def one(s):
             if ctx.rank == 0:
                 x_dev.copy_(x_pin, non_blocking=True)
-            bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
-                C.cast(arrays[s % 8], C.c_void_p), G, x_dev.data_ptr(), n, y_gather.data_ptr(), world * m, n, b,
-                beta, mu, ctx.rank, world, C.byref(cs), ws.ptr(), ws.nbytes, 0, stream.cuda_stream))
+            bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
+                C.cast(arrays[s % 8], C.c_void_p), G, x_dev.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p), world * m,
+                n, b, beta, mu, ctx.rank, world, C.byref(cs), ws.ptr(), ws.nbytes, 0, stream.cuda_stream))
             if ctx.rank == 0:
                 y_host.copy_(y_gather, non_blocking=True)
             stream.synchronize()
@@ -641,8 +656,9 @@ def e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K):
             for s in range(K):
                 one(s)
             e2e_s = time.perf_counter() - t0
-        api = ("bqg_biqgemm_grouped_sharded_f32 per step: rank 0 H2D of the pinned x batch, NCCL broadcast, grouped "
-               "kernel on each rank's rows, NCCL all-gather, rank 0 D2H of the gathered y batch, synchronised")
+        api = ("bqg_biqgemm_grouped_sharded_p2p_f32 per step: rank 0 H2D of the pinned x batch, NCCL broadcast, the "
+               "grouped kernel on each rank's rows storing y into every rank's gather buffer, a 16-byte barrier, "
+               "rank 0 D2H of the gathered y batch, synchronised")
         d2h = world * G * m * b * 4
     e2e_s = ctx.max_over_ranks(e2e_s)
     return {"value": round(world * kb * G * K / e2e_s / 1e9, 3), "unit": "GB/s",

@@ -376,6 +376,32 @@ int bqg_biqgemm_grouped_sharded_f32(const bqg_shard_call* h_calls, size_t count,
                                     const bqg_collectives* coll, void* d_workspace,
                                     size_t workspace_bytes, int pdl, void* stream);
 
+/* The same with the all-gather FUSED into the kernel (north_star's y
+ * assembly over NVLink without a collective on the data): h_y_gather_peers
+ * is a HOST array of nranks device pointers -- every rank's gather buffer
+ * (nranks x count x R x b floats, same layout as above) as mapped in THIS
+ * process (bqg_ipc_*; entry [rank] is the local buffer).  The texture
+ * kernel's finaliser stores each y row into every rank's buffer as its call
+ * completes; a 16-byte-per-rank all-gather through `coll` then orders every
+ * rank's stores before later reads (a barrier).  Shapes the texture form
+ * does not take fall back to the collective all-gather.  Workspace:
+ * bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(). */
+size_t bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta,
+                                                       unsigned mu, size_t count, int nranks);
+int bqg_biqgemm_grouped_sharded_p2p_f32(const bqg_shard_call* h_calls, size_t count, float* d_x,
+                                        size_t x_rows, float* const* h_y_gather_peers, size_t m,
+                                        size_t n, size_t b, unsigned beta, unsigned mu, int rank,
+                                        int nranks, const bqg_collectives* coll, void* d_workspace,
+                                        size_t workspace_bytes, int pdl, void* stream);
+/* Peer buffers across processes: the cudaIpcMemHandle_t (64 opaque bytes)
+ * of the allocation containing d_ptr plus d_ptr's offset in it (any device
+ * pointer, e.g. a caching-allocator tensor); open maps a peer process's
+ * buffer (lazy peer access) and returns the same offset into it; close
+ * unmaps what open mapped. */
+int bqg_ipc_get_handle(void* d_ptr, void* h_handle64, size_t* offset);
+int bqg_ipc_open_handle(const void* h_handle64, size_t offset, void** d_ptr);
+int bqg_ipc_close_handle(void* d_ptr);
+
 #ifdef __cplusplus
 }
 #endif

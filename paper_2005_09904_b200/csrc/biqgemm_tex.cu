@@ -127,6 +127,13 @@ struct TexArgs {
     long long total;  // ncalls * NB * MT units
     float* partial;   // ncalls x NB x (MT*32), fp32
     unsigned* cnt;    // [kStreamMaxGroup] completion counters (zero between launches)
+    // Fused all-gather (row-sharded calls): y rows are also stored at the
+    // same offset from each peer's gather buffer -- NVLink stores into the
+    // other GPUs' memory, issued by the finaliser as each call completes.
+    // npeer = 0: the local y only.  local_base: this rank's gather buffer.
+    int npeer;
+    const float* local_base;
+    float* peer_base[kMaxPeers];
     TexCall calls[kStreamMaxGroup];
 };
 
@@ -391,10 +398,17 @@ __device__ __forceinline__ void fin_chunk(const TexArgs& A, int c, int ch, int l
     }
     float* y = A.calls[c].y + r0;
     const long long left = A.m - r0;
-    y[0] = static_cast<float>(s0);
-    if (left > 1) y[1] = static_cast<float>(s1);
-    if (left > 2) y[2] = static_cast<float>(s2);
-    if (left > 3) y[3] = static_cast<float>(s3);
+    auto put = [&](float* d) {
+        d[0] = static_cast<float>(s0);
+        if (left > 1) d[1] = static_cast<float>(s1);
+        if (left > 2) d[2] = static_cast<float>(s2);
+        if (left > 3) d[3] = static_cast<float>(s3);
+    };
+    put(y);
+    if (A.npeer > 0) {  // the same rows into every peer's gather buffer (fire-and-forget stores)
+        const long long off = y - A.local_base;
+        for (int k = 0; k < A.npeer; ++k) put(A.peer_base[k] + off);
+    }
 }
 
 // One finalisation chunk if any is available: returns false when the queue
@@ -715,7 +729,9 @@ bool tex_stream_applies(long long m, int G, int beta) {
 }
 
 cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
-                               float* ws, bool pdl, cudaStream_t stream) {
+                               float* ws, bool pdl, cudaStream_t stream, const float* local_base,
+                               float* const* peer_base, int npeer) {
+    if (npeer < 0 || npeer > kMaxPeers) return cudaErrorInvalidValue;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -723,6 +739,9 @@ cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_r
     std::vector<TexArgs> buf(1);  // ~12 KiB: keep it off the caller's stack
     TexArgs& A = buf[0];
     A.x_rows = x_rows;
+    A.npeer = npeer;
+    A.local_base = local_base;
+    for (int k = 0; k < kMaxPeers; ++k) A.peer_base[k] = k < npeer ? peer_base[k] : nullptr;
     A.m = m;
     A.NB = (G + 31) / 32;
     A.MT = (m + 31) / 32;

@@ -1612,3 +1612,143 @@ extern "C" int bqg_biqgemm_grouped_sharded_f32(const bqg_shard_call* h_calls, si
     // 3. the rank blocks to every rank
     return coll->allgather(coll->ctx, y_mine, d_y_gather, count * block * sizeof(float), stream);
 }
+
+// ============================================================ fused all-gather over peer memory
+
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no link-time
+// libcuda dependency): the base of the allocation that contains p.
+int allocation_base(void* p, char** base) {
+    using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static Fn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<Fn>(f);
+        cudaGetLastError();
+    });
+    if (!fn) return set_err(BQG_ERR_CUDA, "ipc: cuMemGetAddressRange unavailable");
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "ipc: pointer is not in a device allocation");
+    *base = reinterpret_cast<char*>(b);
+    return BQG_OK;
+}
+}  // namespace
+
+extern "C" int bqg_ipc_get_handle(void* d_ptr, void* h_handle, size_t* offset) {
+    if (!d_ptr || !h_handle || !offset) return set_err(BQG_ERR_INVALID_ARGUMENT, "ipc_get_handle: null pointer");
+    char* base = nullptr;
+    int s = allocation_base(d_ptr, &base);
+    if (s) return s;
+    cudaIpcMemHandle_t hd;
+    BQG_CUDA(cudaIpcGetMemHandle(&hd, base));
+    static_assert(sizeof(hd) <= 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(h_handle, &hd, sizeof(hd));
+    *offset = static_cast<size_t>(static_cast<char*>(d_ptr) - base);
+    return BQG_OK;
+}
+
+extern "C" int bqg_ipc_open_handle(const void* h_handle, size_t offset, void** d_ptr) {
+    if (!h_handle || !d_ptr) return set_err(BQG_ERR_INVALID_ARGUMENT, "ipc_open_handle: null pointer");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, h_handle, sizeof(hd));
+    void* base = nullptr;
+    BQG_CUDA(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+    *d_ptr = static_cast<char*>(base) + offset;
+    return BQG_OK;
+}
+
+extern "C" int bqg_ipc_close_handle(void* d_ptr) {
+    if (!d_ptr) return BQG_OK;
+    char* base = nullptr;
+    int s = allocation_base(d_ptr, &base);
+    if (s) return s;
+    BQG_CUDA(cudaIpcCloseMemHandle(base));
+    return BQG_OK;
+}
+
+namespace {
+constexpr size_t kBarrierBytesPerRank = 16;
+size_t barrier_offset(size_t grouped_ws) { return (grouped_ws + 255) & ~size_t(255); }
+}  // namespace
+
+extern "C" size_t bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta,
+                                                                  unsigned mu, size_t count, int nranks) {
+    const size_t g = bqg_biqgemm_grouped_sharded_workspace_bytes(m, n, b, beta, mu, count, nranks);
+    if (g == 0) return 0;
+    return barrier_offset(g) + kBarrierBytesPerRank * static_cast<size_t>(nranks);
+}
+
+extern "C" int bqg_biqgemm_grouped_sharded_p2p_f32(const bqg_shard_call* h_calls, size_t count, float* d_x,
+                                                   size_t x_rows, float* const* h_y_gather_peers, size_t m, size_t n,
+                                                   size_t b, unsigned beta, unsigned mu, int rank, int nranks,
+                                                   const bqg_collectives* coll, void* d_ws, size_t ws_bytes, int pdl,
+                                                   void* stream) {
+    size_t lo = 0, hi = 0, R = 0;
+    int s = bqg_shard_rows(m, nranks, rank, &lo, &hi, &R);
+    if (s) return s;
+    if (!coll || !coll->broadcast || !coll->allgather)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: collectives missing");
+    if (!d_x || !h_y_gather_peers || (count && !h_calls))
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null pointer");
+    for (int r = 0; r < nranks; ++r)
+        if (!h_y_gather_peers[r]) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null peer buffer %d", r);
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    const size_t gws = bqg_biqgemm_grouped_sharded_workspace_bytes(m, n, b, beta, mu, std::max<size_t>(count, 1), nranks);
+    if (!d_ws || ws_bytes < barrier_offset(gws) + kBarrierBytesPerRank * static_cast<size_t>(nranks))
+        return set_err(BQG_ERR_WORKSPACE, "biqgemm_sharded_p2p: workspace too small");
+    if (count == 0) return BQG_OK;
+    const size_t xs = x_rows * b, block = R * b;
+    float* y_local = h_y_gather_peers[rank];
+    // 1. every call's x from rank 0
+    s = coll->broadcast(coll->ctx, d_x, count * xs * sizeof(float), 0, stream);
+    if (s) return s;
+    // the same decision on every rank (it picks the collective that follows)
+    const bool fused = nranks - 1 <= bqg::kMaxPeers && count >= static_cast<size_t>(bqg::kTexMinGroup) &&
+                       bqg::stream_supported(static_cast<int>(mu), static_cast<int>(beta), static_cast<long long>(b)) &&
+                       bqg::tex_stream_applies(static_cast<long long>(R), static_cast<int>(groups_of(n, mu)),
+                                               static_cast<int>(beta));
+    if (hi > lo) {
+        std::vector<bqg::StreamCall> calls(count);
+        for (size_t i = 0; i < count; ++i) {
+            if (!h_calls[i].d_keys_tiled_shard)
+                return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null keys in call %zu", i);
+            calls[i] = {h_calls[i].d_keys_tiled_shard, h_calls[i].d_alpha_shard, d_x + i * xs,
+                        y_local + (static_cast<size_t>(rank) * count + i) * block};
+        }
+        if (fused) {
+            // 2+3. the grouped texture kernel on this rank's rows; its
+            // finaliser stores every y row into every peer's gather buffer
+            std::vector<float*> peers;
+            for (int r = 0; r < nranks; ++r)
+                if (r != rank) peers.push_back(h_y_gather_peers[r]);
+            cudaError_t e = bqg::launch_biqgemm_tex(calls.data(), static_cast<int>(count), static_cast<long long>(x_rows),
+                                                    static_cast<int>(hi - lo), static_cast<int>(groups_of(n, mu)),
+                                                    static_cast<int>(beta), static_cast<float*>(d_ws), pdl != 0,
+                                                    as_stream(stream), y_local, peers.data(),
+                                                    static_cast<int>(peers.size()));
+            if (e != cudaSuccess) return cuda_err(e, "biqgemm grouped p2p kernel");
+        } else {
+            std::vector<bqg_call> gc(count);
+            for (size_t i = 0; i < count; ++i) gc[i] = {calls[i].keys, calls[i].alpha, calls[i].x, calls[i].y};
+            s = bqg_biqgemm_grouped_f32(gc.data(), count, x_rows, hi - lo, n, b, beta, mu, d_ws, gws, pdl, stream);
+            if (s) return s;
+        }
+    }
+    if (!fused) {  // shapes the texture form does not take: the gather through the collectives
+        float* y_mine = y_local + static_cast<size_t>(rank) * count * block;
+        return coll->allgather(coll->ctx, y_mine, y_local, count * block * sizeof(float), stream);
+    }
+    // 4. a barrier (an all-gather of 16 bytes per rank): every rank's kernel
+    //    -- and with it every peer store into this rank's buffer -- is
+    //    complete before work queued after this call reads y
+    char* bar = static_cast<char*>(d_ws) + barrier_offset(gws);
+    return coll->allgather(coll->ctx, bar + static_cast<size_t>(rank) * kBarrierBytesPerRank, bar,
+                           kBarrierBytesPerRank, stream);
+}

@@ -64,8 +64,13 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
 // tex_stream_applies (texel range) unless BQG_STREAM_IMPL=tma.
 bool tex_stream_applies(long long m, int G, int beta);
 constexpr int kTexMinGroup = 4;
+// peer_base / npeer (<= kMaxPeers): the finaliser also stores every y row at
+// the same offset from local_base in each peer gather buffer (fused
+// all-gather over NVLink; npeer = 0: local y only).
+constexpr int kMaxPeers = 8;
 cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
-                               float* ws, bool pdl, cudaStream_t stream);
+                               float* ws, bool pdl, cudaStream_t stream, const float* local_base = nullptr,
+                               float* const* peer_base = nullptr, int npeer = 0);
 
 // Single-call latency form (biqgemm_latency.cu): b == 1, mu == 8, beta <= 4,
 // NB in {1,2,4,8,16}; one kernel, in-cluster push reduction.  *used = false

@@ -339,3 +339,90 @@ class ShardedGroup:
             self.beta, self.mu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
             bq._stream(stream)))
         return self.assemble(y_gather)
+
+
+class PeerGather:
+    """One gather buffer per rank that every rank can store into: a torch
+    tensor here, its CUDA IPC handle exchanged over torch.distributed, the
+    peers' buffers mapped into this process (bqg_ipc_*).  `ptrs` is the
+    host pointer array bqg_biqgemm_grouped_sharded_p2p_f32 takes (entry
+    [rank] = the local buffer)."""
+
+    def __init__(self, shape, rank: int, world: int, group=None, device=None):
+        from . import _capi
+
+        self._capi = _capi
+        lib = _capi.lib
+        self.tensor = torch.zeros(shape, dtype=torch.float32, device=device)
+        torch.cuda.synchronize(self.tensor.device)
+        h = (C.c_char * 64)()
+        off = C.c_size_t()
+        _capi.check(lib.bqg_ipc_get_handle(C.c_void_p(self.tensor.data_ptr()), h, C.byref(off)))
+        mine = (bytes(h), off.value)
+        allh = [None] * world
+        if world > 1:
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self.opened = []
+        ptrs = []
+        for r in range(world):
+            if r == rank:
+                ptrs.append(self.tensor.data_ptr())
+                continue
+            p = C.c_void_p()
+            hb, o = allh[r]
+            _capi.check(lib.bqg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb), o, C.byref(p)))
+            self.opened.append(p.value)
+            ptrs.append(p.value)
+        self.ptrs = (C.c_void_p * world)(*ptrs)
+
+    def close(self):
+        for p in self.opened:
+            self._capi.lib.bqg_ipc_close_handle(C.c_void_p(p))
+        self.opened = []
+
+
+class ShardedGroupP2P(ShardedGroup):
+    """ShardedGroup with the all-gather fused into the grouped kernel: each
+    rank's finaliser stores its y rows straight into every rank's gather
+    buffer (NVLink peer stores; bqg_biqgemm_grouped_sharded_p2p_f32), and a
+    16-byte-per-rank all-gather is the only collective on the y side."""
+
+    def __init__(self, shards: list, b: int = 1, group=None):
+        super().__init__(shards)
+        self.peer = PeerGather((self.world, len(self), self.plan.max_rows, b), self.rank, self.world, group=group,
+                               device=self.device)
+        self.b = b
+
+    def gather_buffer(self, b: int) -> torch.Tensor:
+        if b != self.b:
+            raise ValueError(f"ShardedGroupP2P: made for b = {self.b}")
+        return self.peer.tensor
+
+    def forward_device(self, x: torch.Tensor, y_gather: torch.Tensor = None, pdl: bool = False,
+                       stream=None) -> torch.Tensor:
+        bq = self.bq
+        count, x_rows, b = x.shape
+        y_gather = self.peer.tensor if y_gather is None else y_gather
+        if y_gather.data_ptr() != self.peer.tensor.data_ptr():
+            raise ValueError("ShardedGroupP2P: y lives in the peer-mapped gather buffer (gather_buffer())")
+        if count != len(self) or b != self.b:
+            raise ValueError("ShardedGroupP2P: x must be [count, n, b] for this group")
+        if not (x.dtype == torch.float32 and x.is_contiguous() and x.device == self.device):
+            raise ValueError("ShardedGroupP2P: x must be a contiguous float32 tensor on this rank's device")
+        if b not in self._ws:
+            self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(
+                self.m, self.n, b, self.beta, self.mu, count, self.world)), device=self.device)
+        ws = self._ws[b]
+        if isinstance(self.coll_provider, TorchCollectives):
+            self.coll_provider.register(x, y_gather, ws.buf)
+        coll = self.coll_provider.collectives()
+        bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
+            C.cast(self._arr, C.c_void_p), count, x.data_ptr(), x_rows, C.cast(self.peer.ptrs, C.c_void_p), self.m,
+            self.n, b, self.beta, self.mu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
+            bq._stream(stream)))
+        return self.assemble(y_gather)
+
+    def close(self):
+        self.peer.close()

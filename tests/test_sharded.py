@@ -212,6 +212,66 @@ def _grouped_worker(rank, world, port, m, n, beta, count, out_q):
         dist.destroy_process_group()
 
 
+def _p2p_worker(rank, world, port, m, n, beta, count, out_q):
+    """One rank of the FUSED all-gather (bqg_biqgemm_grouped_sharded_p2p_f32):
+    the ranks are processes on one GPU, their gather buffers mapped into each
+    other through CUDA IPC; gloo carries x's broadcast and the barrier."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2005_09904_b200.biqgemm as bq
+        from paper_2005_09904_b200.sharded import ShardedGroupP2P, ShardedLinear, TorchCollectives
+
+        coll = TorchCollectives()
+        ws_ = [bq.random_uniform(m, n, 100 + i) for i in range(count)]
+        shards = [ShardedLinear.from_weights(w, beta, 8, rank, world, coll) for w in ws_]
+        grp = ShardedGroupP2P(shards, b=1)
+        ok, diff = True, 0.0
+        for rep in range(2):
+            x_h = np.stack([bq.random_normal(n, 1, 200 + i + 50 * rep) for i in range(count)])
+            x = torch.from_numpy(x_h).cuda() if rank == 0 else torch.zeros((count, n, 1), device="cuda")
+            grp.gather_buffer(1).fill_(float("nan"))
+            dist.barrier()
+            y = grp.forward_device(x).cpu().numpy()
+            for i, w in enumerate(ws_):
+                full = bq.PackedLinear.from_weights(w, beta, 8)
+                y_full = full.forward(x_h[i])
+                ok = ok and bool(np.array_equal(y[i], y_full))
+                diff = max(diff, float(np.nanmax(np.abs(y[i] - y_full))) if not np.isnan(y[i]).all() else 1e30)
+                full.close()
+            dist.barrier()
+        grp.close()
+        for s in shards:
+            s.close()
+        out_q.put((rank, ok, diff))
+    except Exception as e:
+        out_q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,m,n,beta,count", [(2, 4096, 4096, 3, 6), (3, 1000, 777, 2, 5)])
+def test_fused_allgather_peer_stores_single_gpu(cuda, world, m, n, beta, count):
+    """The all-gather fused into the grouped kernel (peer stores into every
+    rank's IPC-mapped gather buffer, then a 16-byte barrier): every rank's
+    assembled y == the unsharded y, bit for bit, twice in a row."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, portn, m, n, beta, count, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, diff in res:
+        assert ok, f"rank {rank}: {diff}"
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,m,n,beta,count", [(2, 4096, 4096, 3, 6), (3, 1000, 777, 2, 5)])
 def test_native_grouped_sharded_single_gpu_gloo(cuda, world, m, n, beta, count):
