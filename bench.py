@@ -34,10 +34,11 @@ pipelined inside the call), wall-clock timed.
 N>1 (torchrun, one GPU per rank, NCCL): the north-star decomposition through
 the sharded C-ABI entries.  b = 1 configs weak-scale: the layer has N*m rows,
 each rank owns an m-row shard of every call, and a step is one
-bqg_biqgemm_grouped_sharded_f32 (NCCL broadcast of the G inputs -> grouped
-kernel on the rank's rows -> NCCL all-gather of the G outputs).  The line
+bqg_biqgemm_grouped_sharded_p2p_f32 (NCCL broadcast of the G inputs ->
+grouped kernel on the rank's rows, its finaliser storing every y row into
+every rank's IPC-mapped gather buffer -> a 16-byte NCCL barrier).  The line
 also carries `c5_strong`: BASELINE configs[4] (65536x8192, q2, b8) strong-
-scaled over the N ranks through bqg_biqgemm_sharded_f32, with T(1) measured
+scaled over the N ranks through bqg_biqgemm_sharded_p2p_f32, with T(1) measured
 on rank 0's GPU alone in the same run, the efficiency T(1)/(N*T(N)) and a
 bitwise check of y against T(1)'s.  `--config C5` makes that the main line.
 
@@ -786,17 +787,21 @@ def c5_time(ctx, bq, keys, alpha, x, rank, world, coll, K, W):
     t0 = bq.tile_keys(torch.from_numpy(np.ascontiguousarray(keys[:, lo:hi])).to(dev), n, mu)
     a0 = torch.from_numpy(np.ascontiguousarray(alpha[:, lo:hi])).to(dev)
     tiled, alphas, copies = rotating_copies(ctx, t0, a0)
+    from paper_2005_09904_b200.sharded import PeerGather
+
     x_dev = torch.from_numpy(x).to(dev)
-    y_gather = torch.empty((world * R, b), device=dev)
-    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_workspace_bytes(m, n, b, beta, mu, world)), device=dev)
+    peer = PeerGather((world * R, b), rank, world, device=dev)  # every rank's gather buffer, IPC-mapped
+    y_gather = peer.tensor
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_p2p_workspace_bytes(m, n, b, beta, mu, world)), device=dev)
     if hasattr(coll, "register"):
-        coll.register(x_dev, y_gather)
+        coll.register(x_dev, y_gather, ws.buf)
     cs = coll.collectives()
 
     def call(i):
-        bq.check(bq.lib.bqg_biqgemm_sharded_f32(tiled[i % copies].data_ptr(), alphas[i % copies].data_ptr(),
-                                                x_dev.data_ptr(), n, y_gather.data_ptr(), m, n, b, beta, mu, rank,
-                                                world, C.byref(cs), ws.ptr(), ws.nbytes, stream.cuda_stream))
+        bq.check(bq.lib.bqg_biqgemm_sharded_p2p_f32(tiled[i % copies].data_ptr(), alphas[i % copies].data_ptr(),
+                                                    x_dev.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p), m, n, b,
+                                                    beta, mu, rank, world, C.byref(cs), ws.ptr(), ws.nbytes,
+                                                    stream.cuda_stream))
 
     def compute(i):
         bq.biqgemm_device(tiled[i % copies], alphas[i % copies], x_dev, y_gather[rank * R: rank * R + (hi - lo)],
@@ -811,6 +816,10 @@ def c5_time(ctx, bq, keys, alpha, x, rank, world, coll, K, W):
     sub = ctx if world == ctx.world else _Solo(ctx)
     e2e = float(np.median([sub.time_ms(lambda: [call(i) for i in range(K)]) for _ in range(3)])) / K
     comp = float(np.median([sub.time_ms(lambda: [compute(i) for i in range(K)]) for _ in range(3)])) / K
+    stream.synchronize()
+    if world > 1:
+        ctx.barrier()  # no rank unmaps a peer buffer another rank may still store into
+    peer.close()
     return e2e, comp, digest
 
 
@@ -842,13 +851,14 @@ def c5_strong(ctx, bq, args):
     keys, alpha, x = c5_inputs(bq)
     kb = key_bytes(m, n, beta, mu)
     out = {"workload": f"C5 m={m} n={n} q={beta} mu={mu} b={b}", "steps": K,
-           "step": "one row-sharded call: NCCL broadcast of x -> fused kernel on the rank's rows -> NCCL all-gather "
-                   "of y (bqg_biqgemm_sharded_f32)",
+           "step": "one row-sharded call: NCCL broadcast of x -> the two-kernel form on the rank's rows, its "
+                   "finaliser storing y into every rank's IPC-mapped gather buffer -> 16-byte NCCL barrier "
+                   "(bqg_biqgemm_sharded_p2p_f32)",
            "data": "seeded random keys/alpha (identical on every rank), x = random_normal(n,b,0x5EED+1)"}
     t1 = comp1 = None
     digest1 = None
     if ctx.rank == 0:
-        solo = NcclComm(0, 1) if (ctx.world == 1 or ctx.backend == "nccl") else None
+        solo = NcclComm(0, 1) if bq.lib.bqg_nccl_available() else None  # a 1-rank communicator
         if solo is not None:
             t1, comp1, digest1 = c5_time(ctx, bq, keys, alpha, x, 0, 1, solo, K, W)
             solo.close()

@@ -393,6 +393,22 @@ int bqg_biqgemm_grouped_sharded_p2p_f32(const bqg_shard_call* h_calls, size_t co
                                         size_t n, size_t b, unsigned beta, unsigned mu, int rank,
                                         int nranks, const bqg_collectives* coll, void* d_workspace,
                                         size_t workspace_bytes, int pdl, void* stream);
+/* One row-sharded call with the all-gather fused into the kernels (the
+ * north_star C5 decomposition): broadcast x, then the two-kernel form on this
+ * rank's rows -- every shard count takes that form, so y is bitwise
+ * independent of nranks -- whose finaliser stores each y value into every
+ * rank's gather buffer (h_y_gather_peers as above; each buffer nranks x R x b
+ * floats, the first m*b are y), then the 16-byte barrier.  b = 1 shapes the
+ * latency / stream forms serve, and shapes the two-kernel form does not take,
+ * run the rank's rows with bqg_biqgemm_f32 and gather through `coll`.
+ * Workspace: bqg_biqgemm_sharded_p2p_workspace_bytes(). */
+size_t bqg_biqgemm_sharded_p2p_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                               int nranks);
+int bqg_biqgemm_sharded_p2p_f32(const uint8_t* d_keys_tiled_shard, const float* d_alpha_shard, float* d_x,
+                                size_t x_rows, float* const* h_y_gather_peers, size_t m, size_t n,
+                                size_t b, unsigned beta, unsigned mu, int rank, int nranks,
+                                const bqg_collectives* coll, void* d_workspace, size_t workspace_bytes,
+                                void* stream);
 /* Peer buffers across processes: the cudaIpcMemHandle_t (64 opaque bytes)
  * of the allocation containing d_ptr plus d_ptr's offset in it (any device
  * pointer, e.g. a caching-allocator tensor); open maps a peer process's

@@ -323,6 +323,15 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
 #pragma unroll
     for (int c = 0; c < COLS; ++c)
         if (ct * BT + cc * COLS + c < p.b) yr[c] = static_cast<float>(y[c]);
+    // fused all-gather: the same values into every peer's gather buffer (NVLink stores)
+#pragma unroll 1
+    for (int k = 0; k < kMaxPeers; ++k) {
+        if (k >= p.npeer) break;
+        float* py = p.peer_y[k] + (yr - p.peer_local);
+#pragma unroll
+        for (int c = 0; c < COLS; ++c)
+            if (ct * BT + cc * COLS + c < p.b) py[c] = static_cast<float>(y[c]);
+    }
 }
 
 #ifndef BQG_FAST_NW
@@ -530,6 +539,25 @@ cudaError_t launch_biqgemm_fast(const QueryParams& p_in, int mu, bool pdl, cudaS
         const StreamCall call{p.keys, p.alpha, p.x, p.y};
         return launch_biqgemm_stream(&call, 1, p.x_rows, p.m, p.G, p.beta, p.ws, pdl, stream);
     }
+    return launch_biqgemm_twokernel(p, mu, pdl, stream);
+}
+
+bool twokernel_supported(int mu, int beta, long long b) {
+    if (mu < 1 || mu > 8 || beta < 1) return false;
+    FastPlan pl{};
+    return ring_shape(mu, pick_bt(b), beta, pl) && pl.R >= 2;
+}
+
+cudaError_t launch_biqgemm_twokernel(const QueryParams& p_in, int mu, bool pdl, cudaStream_t stream) {
+    static const int debug_flags = [] {
+        const char* e = getenv("BQG_DEBUG_FLAGS");
+        return e ? atoi(e) : 0;
+    }();
+    if (p_in.npeer < 0 || p_in.npeer > kMaxPeers) return cudaErrorInvalidValue;
+    const int sms = device_sms(current_device());
+    QueryParams p = p_in;
+    p.debug = debug_flags;
+    p.bt = pick_bt(p.b);
     const FastPlan plan = make_plan(p.m, p.G, p.beta, p.b, mu, sms);
     if (plan.R < 2) return cudaErrorInvalidValue;  // beta too large for a two-stage key ring
     const int bt = pick_bt(p.b);

@@ -1752,3 +1752,71 @@ extern "C" int bqg_biqgemm_grouped_sharded_p2p_f32(const bqg_shard_call* h_calls
     return coll->allgather(coll->ctx, bar + static_cast<size_t>(rank) * kBarrierBytesPerRank, bar,
                            kBarrierBytesPerRank, stream);
 }
+
+extern "C" size_t bqg_biqgemm_sharded_p2p_workspace_bytes(size_t m, size_t n, size_t b, unsigned beta, unsigned mu,
+                                                          int nranks) {
+    const size_t g = bqg_biqgemm_sharded_workspace_bytes(m, n, b, beta, mu, nranks);
+    if (g == 0) return 0;
+    return barrier_offset(g) + kBarrierBytesPerRank * static_cast<size_t>(nranks);
+}
+
+extern "C" int bqg_biqgemm_sharded_p2p_f32(const uint8_t* d_keys_tiled_shard, const float* d_alpha_shard, float* d_x,
+                                           size_t x_rows, float* const* h_y_gather_peers, size_t m, size_t n,
+                                           size_t b, unsigned beta, unsigned mu, int rank, int nranks,
+                                           const bqg_collectives* coll, void* d_ws, size_t ws_bytes, void* stream) {
+    size_t lo = 0, hi = 0, R = 0;
+    int s = bqg_shard_rows(m, nranks, rank, &lo, &hi, &R);
+    if (s) return s;
+    if (!coll || !coll->broadcast || !coll->allgather)
+        return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: collectives missing");
+    if (!d_x || !h_y_gather_peers) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null pointer");
+    for (int r = 0; r < nranks; ++r)
+        if (!h_y_gather_peers[r]) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null peer buffer %d", r);
+    s = check_mu(mu, "biqgemm");
+    if (s) return s;
+    s = check_x(x_rows, b, n, mu, "biqgemm");
+    if (s) return s;
+    const size_t gws = bqg_biqgemm_sharded_workspace_bytes(m, n, b, beta, mu, nranks);
+    if (!d_ws || gws == 0 || ws_bytes < barrier_offset(gws) + kBarrierBytesPerRank * static_cast<size_t>(nranks))
+        return set_err(BQG_ERR_WORKSPACE, "biqgemm_sharded_p2p: workspace too small");
+    float* y_local = h_y_gather_peers[rank];
+    float* y_mine = y_local + static_cast<size_t>(rank) * R * b;
+    // 1. x from rank 0 to every rank
+    s = coll->broadcast(coll->ctx, d_x, x_rows * b * sizeof(float), 0, stream);
+    if (s) return s;
+    // the same decision on every rank (it picks the collective that follows):
+    // shapes the two-kernel form takes, except the b = 1 shapes the latency /
+    // stream forms serve
+    const bool fused = nranks - 1 <= bqg::kMaxPeers && mu <= 8 &&
+                       !bqg::stream_supported(static_cast<int>(mu), static_cast<int>(beta), static_cast<long long>(b)) &&
+                       bqg::twokernel_supported(static_cast<int>(mu), static_cast<int>(beta), static_cast<long long>(b));
+    if (!fused) {  // the rank's rows, then the gather through the collectives
+        if (hi > lo) {
+            s = bqg_biqgemm_f32(d_keys_tiled_shard, d_alpha_shard, d_x, x_rows, y_mine, hi - lo, n, b, beta, mu, d_ws,
+                                gws, 0, stream);
+            if (s) return s;
+        }
+        return coll->allgather(coll->ctx, y_mine, y_local, R * b * sizeof(float), stream);
+    }
+    if (hi > lo) {
+        if (!d_keys_tiled_shard) return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm_sharded: null keys");
+        if (hi - lo > 0x7fffffff || b > 0x7fffffff)
+            return set_err(BQG_ERR_INVALID_ARGUMENT, "biqgemm: dimension too large");
+        BQG_NEED_DEVICE();
+        // 2+3. the two-kernel form on this rank's rows (every shard count
+        // takes the same form, so y is bitwise independent of nranks); its
+        // finaliser stores every y value into every peer's gather buffer
+        bqg::QueryParams p = make_params(d_keys_tiled_shard, d_alpha_shard, d_x, x_rows, y_mine, hi - lo, n, b, beta,
+                                         mu, d_ws);
+        p.peer_local = y_local;
+        for (int r = 0; r < nranks; ++r)
+            if (r != rank) p.peer_y[p.npeer++] = h_y_gather_peers[r];
+        cudaError_t e = bqg::launch_biqgemm_twokernel(p, static_cast<int>(mu), false, as_stream(stream));
+        if (e != cudaSuccess) return cuda_err(e, "biqgemm sharded p2p kernels");
+    }
+    // 4. the barrier: every rank's kernels, and their peer stores into this
+    //    rank's buffer, are complete before work queued after this call reads y
+    char* bar = static_cast<char*>(d_ws) + barrier_offset(gws);
+    return coll->allgather(coll->ctx, bar + static_cast<size_t>(rank) * kBarrierBytesPerRank, bar,
+                           kBarrierBytesPerRank, stream);
+}

@@ -34,6 +34,11 @@ constexpr int kStreamMaxGroup = 512;  // calls per launch (kernel-parameter arra
 // counters.
 constexpr size_t kTexCounterBytes = kStreamMaxGroup * sizeof(unsigned);
 
+// Fused all-gather (biqgemm_tex.cu's finaliser, the two-kernel form's
+// finalize_kernel): every y row is also stored at the same offset from a
+// local base in each of up to kMaxPeers peer gather buffers.
+constexpr int kMaxPeers = 8;
+
 struct QueryParams {
     const uint8_t* keys;    // tiled
     const float* alpha;     // beta x m or nullptr (plane mode: alpha = 1)
@@ -45,6 +50,10 @@ struct QueryParams {
     int m, G, NB, MT, beta, b, cpb;
     int bt;     // fast form: input columns per column tile (1, 2 or 4)
     int debug;  // profiling switches (BQG_DEBUG_FLAGS); 0 in production
+    // two-kernel form only: y(r, c) is also stored at peer_y[k] + (&y(r, c) - peer_local)
+    int npeer;
+    const float* peer_local;
+    float* peer_y[kMaxPeers];
 };
 
 // Grouped ("stream") form: a group of independent calls sharing (m, n, beta,
@@ -67,7 +76,6 @@ constexpr int kTexMinGroup = 4;
 // peer_base / npeer (<= kMaxPeers): the finaliser also stores every y row at
 // the same offset from local_base in each peer gather buffer (fused
 // all-gather over NVLink; npeer = 0: local y only).
-constexpr int kMaxPeers = 8;
 cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
                                float* ws, bool pdl, cudaStream_t stream, const float* local_base = nullptr,
                                float* const* peer_base = nullptr, int npeer = 0);
@@ -105,6 +113,11 @@ cudaError_t launch_tile_keys(const uint8_t* keys, long long m, long long groups,
 // Fast path (mu <= 8): fused LUT build -> query -> alpha epilogue.
 // Tries the single-kernel cluster form first, else two PDL-chained kernels.
 cudaError_t launch_biqgemm_fast(const QueryParams& p, int mu, bool pdl, cudaStream_t stream);
+// The two-kernel form (form 3) directly, whatever fast_form would pick: the
+// row-sharded entries use it for every shard so y is bitwise the same for any
+// shard count, and its finaliser honours p.npeer / p.peer_y.
+bool twokernel_supported(int mu, int beta, long long b);
+cudaError_t launch_biqgemm_twokernel(const QueryParams& p, int mu, bool pdl, cudaStream_t stream);
 // Single-kernel form with an in-cluster reduction; *used = false when the
 // device cannot co-schedule the cluster (caller falls back).
 cudaError_t launch_biqgemm_cluster(const QueryParams& p, int mu, bool pdl, cudaStream_t stream, bool* used);

@@ -426,3 +426,57 @@ class ShardedGroupP2P(ShardedGroup):
 
     def close(self):
         self.peer.close()
+
+
+class ShardedLinearP2P(ShardedLinear):
+    """ShardedLinear with the all-gather fused into the kernels
+    (bqg_biqgemm_sharded_p2p_f32): the two-kernel form's finaliser stores
+    every y value into every rank's IPC-mapped gather buffer, then a 16-byte
+    barrier.  The gather buffer is fixed at construction (b columns)."""
+
+    def __init__(self, shard_layer, m: int, n: int, beta: int, mu: int, rank: int, world: int, collectives,
+                 b: int = 1, group=None, device=None):
+        super().__init__(shard_layer, m, n, beta, mu, rank, world, collectives, device=device)
+        self.b = b
+        self.peer = PeerGather((world * self.plan.max_rows, b), rank, world, group=group, device=self.device)
+
+    @classmethod
+    def from_weights(cls, w_full, beta, mu, rank, world, collectives, b: int = 1, group=None):
+        base = ShardedLinear.from_weights(w_full, beta, mu, rank, world, collectives)
+        return cls(base.layer, base.m, base.n, beta, mu, rank, world, collectives, b=b, group=group)
+
+    def gather_buffer(self, b: int) -> torch.Tensor:
+        if b != self.b:
+            raise ValueError(f"ShardedLinearP2P: made for b = {self.b}")
+        return self.peer.tensor
+
+    def workspace(self, b: int):
+        if b not in self._ws:
+            bq = self.bq
+            self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_p2p_workspace_bytes(
+                self.m, self.n, b, self.beta, self.mu, self.world)), device=self.device)
+        return self._ws[b]
+
+    def forward_device(self, x: torch.Tensor, y_gather: torch.Tensor = None, stream=None) -> torch.Tensor:
+        bq = self.bq
+        x_rows, b = x.shape
+        y_gather = self.peer.tensor if y_gather is None else y_gather
+        if y_gather.data_ptr() != self.peer.tensor.data_ptr() or b != self.b:
+            raise ValueError("ShardedLinearP2P: y lives in the peer-mapped gather buffer (gather_buffer(b))")
+        if not (x.dtype == torch.float32 and x.is_contiguous() and x.device == self.device):
+            raise ValueError("ShardedLinearP2P: x must be a contiguous float32 tensor on this rank's device")
+        ws = self.workspace(b)
+        if isinstance(self.coll_provider, TorchCollectives):
+            self.coll_provider.register(x, y_gather, ws.buf)
+        keys = self.layer.device_tiled_keys if self.layer is not None else None
+        alpha = self.layer.device_alpha if self.layer is not None else None
+        coll = self.coll_provider.collectives()
+        bq.check(bq.lib.bqg_biqgemm_sharded_p2p_f32(keys, alpha, x.data_ptr(), x_rows,
+                                                    C.cast(self.peer.ptrs, C.c_void_p), self.m, self.n, b,
+                                                    self.beta, self.mu, self.rank, self.world, C.byref(coll),
+                                                    ws.ptr(), ws.nbytes, bq._stream(stream)))
+        return y_gather[: self.m]
+
+    def close(self):
+        self.peer.close()
+        super().close()

@@ -1,8 +1,10 @@
 """bench.py --gpus 2 under torchrun on ONE GPU (gloo collectives behind the
 bqg_collectives vtable, both ranks on cuda:0): the N > 1 control flow the
 driver's scaling run uses -- the grouped row-sharded step through
-bqg_biqgemm_grouped_sharded_f32, the max-over-ranks timing, the C5 strong-
-scaling leg through bqg_biqgemm_sharded_f32 -- runs to one JSON line."""
+bqg_biqgemm_grouped_sharded_p2p_f32 (peer stores into IPC-mapped gather
+buffers), the max-over-ranks timing, the C5 strong-scaling leg through
+bqg_biqgemm_sharded_p2p_f32 with y compared bitwise against T(1) -- runs to
+one JSON line."""
 import json
 import os
 import socket
@@ -37,3 +39,4 @@ def test_bench_two_ranks_one_gpu(cuda):
     assert d["parity_rel_fro"] <= 1e-5
     c5 = d["c5_strong"]
     assert c5["n"] == 2 and c5["tN_ms"] > 0
+    assert c5["y_bitwise_equal_to_t1"] is True

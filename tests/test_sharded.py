@@ -272,6 +272,63 @@ def test_fused_allgather_peer_stores_single_gpu(cuda, world, m, n, beta, count):
         assert ok, f"rank {rank}: {diff}"
 
 
+def _p2p_single_worker(rank, world, port, m, n, beta, b, out_q):
+    """One rank of the single-call fused all-gather
+    (bqg_biqgemm_sharded_p2p_f32, the north_star C5 decomposition): processes
+    on one GPU, gather buffers IPC-mapped, gloo for x and the barrier."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2005_09904_b200.biqgemm as bq
+        from paper_2005_09904_b200.sharded import ShardedLinearP2P, TorchCollectives
+
+        w = bq.random_uniform(m, n, 91)
+        sh = ShardedLinearP2P.from_weights(w, beta, 8, rank, world, TorchCollectives(), b=b)
+        full = bq.PackedLinear.from_weights(w, beta, 8)
+        ok, diff = True, 0.0
+        for rep in range(2):
+            x_h = bq.random_normal(n, b, 92 + rep)
+            x = torch.from_numpy(x_h).cuda() if rank == 0 else torch.zeros((n, b), device="cuda")
+            sh.gather_buffer(b).fill_(float("nan"))
+            dist.barrier()
+            y = sh.forward_device(x).cpu().numpy()
+            y_full = full.forward(x_h)
+            ok = ok and bool(np.array_equal(y, y_full))
+            diff = max(diff, float(np.nanmax(np.abs(y - y_full))) if not np.isnan(y).all() else 1e30)
+            dist.barrier()
+        full.close()
+        sh.close()
+        out_q.put((rank, ok, diff))
+    except Exception as e:
+        out_q.put((rank, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,m,n,beta,b", [(2, 4096, 4096, 2, 8), (3, 1000, 777, 2, 5), (2, 3000, 1024, 3, 16),
+                                              (3, 1000, 777, 2, 2), (2, 4096, 4096, 3, 1)])
+def test_fused_allgather_single_call_single_gpu(cuda, world, m, n, beta, b):
+    """bqg_biqgemm_sharded_p2p_f32: the two-kernel finaliser stores every y
+    value into every rank's gather buffer; each rank's y == the unsharded
+    layer's (which takes the same two-kernel form at these shapes; b = 1 takes
+    the collective fallback), bit for bit, twice in a row."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    portn = _free_port()
+    procs = [ctx.Process(target=_p2p_single_worker, args=(r, world, portn, m, n, beta, b, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, diff in res:
+        assert ok, f"rank {rank}: {diff}"
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,m,n,beta,count", [(2, 4096, 4096, 3, 6), (3, 1000, 777, 2, 5)])
 def test_native_grouped_sharded_single_gpu_gloo(cuda, world, m, n, beta, count):
