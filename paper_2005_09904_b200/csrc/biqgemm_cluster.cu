@@ -79,7 +79,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     };
     unsigned char* stages = place(STAGE_AREA);
     float* psum = reinterpret_cast<float*>(place(kPSUM));
-    float* xs = reinterpret_cast<float*>(place(32 * MU * BT * 4));  // staged x tile of the current segment
+    float* xs = reinterpret_cast<float*>(place(xs_words(MU, BT) * 4));  // staged x tile of the current segment
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + R * STAGE_BYTES);
     uint64_t* empty = full + R;
 
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
             for (int k = 0; k < XPT; ++k) {
                 const int idx = threadIdx.x + k * NW * 32;
-                if (idx < XT) xs[idx] = xr[k];
+                if (idx < XT) xs[xs_slot<MU, BT>(idx)] = xr[k];
             }
             named_bar_sync(1, NW * 32);
             if (sg + 1 < nseg) load_x(sg + 1);
@@ -333,7 +333,7 @@ size_t cluster_smem_bytes() {
     const size_t lut = static_cast<size_t>(1u << MU) * LutGeom<BT>::KROW * 4;
     const size_t stages = static_cast<size_t>(kCR) * kCNW * 1024 + 2 * kCR * sizeof(uint64_t);
     // BT <= 2 aligns the LUT to 64 KiB inside the allocation (<= 64 KiB - 1 slack)
-    return (LutGeom<BT>::PRMT ? 65535 : 0) + lut + stages + kPSUM + 32 * MU * BT * 4;
+    return (LutGeom<BT>::PRMT ? 65535 : 0) + lut + stages + kPSUM + xs_words(MU, BT) * 4;
 }
 
 template <int MU, int BT>

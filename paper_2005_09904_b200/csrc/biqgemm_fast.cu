@@ -45,7 +45,9 @@
 namespace bqg {
 
 // Per-CTA timeline for profiling (BQG_DEBUG_FLAGS & 2): globaltimer ns at
-// start, after the LUT build, after the query, end; smid; clock64 at start/end.
+// start (0), after griddepcontrol.wait (1), first segment's LUT built (2),
+// first key stage landed (3), query done (4); smid (5); the last segment's
+// start after the drain barrier (6) and its LUT built (7), 0 for one segment.
 // Off in production (one predicated branch per CTA).
 __device__ unsigned long long g_timeline[8192][8];
 
@@ -99,14 +101,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
     unsigned char* stages = smem + LUT_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(R) * STAGE_BYTES);
     uint64_t* empty = full + kMaxStages;
-    float* xs = reinterpret_cast<float*>(empty + kMaxStages);  // staged x tile (32*MU x BT)
+    float* xs = reinterpret_cast<float*>(empty + kMaxStages);  // staged x tile (xs_words)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool tl = (p.debug & 2) && threadIdx.x == 0 && blockIdx.x < 8192;
     if (tl) {
         g_timeline[blockIdx.x][0] = gtimer();
         g_timeline[blockIdx.x][5] = smid();
-        g_timeline[blockIdx.x][6] = clock64();
+        g_timeline[blockIdx.x][6] = g_timeline[blockIdx.x][7] = 0;
     }
     pdl_launch_dependents();
 
@@ -184,16 +186,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
         const int seg_end = min(cend, pbase + plan.cpp);
         const int gb = pair / plan.CT, ct = pair - gb * plan.CT;
         if (seg != cbeg) named_bar_sync(1, NW * 32);  // previous segment done with the LUT and x tile
+        if (tl && seg != cbeg) g_timeline[blockIdx.x][6] = gtimer();
 #pragma unroll
         for (int k = 0; k < XPT; ++k) {
             const int idx = threadIdx.x + k * NW * 32;
-            if (idx < XT) xs[idx] = xr[k];
+            if (idx < XT) xs[xs_slot<MU, BT>(idx)] = xr[k];
         }
         named_bar_sync(1, NW * 32);
         if (seg_end < cend) load_x(seg_end / plan.cpp);  // the next segment's x, in flight during this one
         build_bank_owned_tables_smem<MU, NW, BT, LutGeom<BT>::KROW>(lut, xs, warp, lane);
         named_bar_sync(1, NW * 32);
-        if (tl) g_timeline[blockIdx.x][2] = gtimer();
+        if (tl) g_timeline[blockIdx.x][seg == cbeg ? 2 : 7] = gtimer();
 
         const int lo = seg - pbase, hi = seg_end - pbase;
         for (int t0 = lo; t0 < hi; t0 += TPS, ++sc) {
@@ -242,10 +245,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
         }
         seg = seg_end;
     }
-    if (tl) {
-        g_timeline[blockIdx.x][4] = gtimer();
-        g_timeline[blockIdx.x][7] = clock64();
-    }
+    if (tl) g_timeline[blockIdx.x][4] = gtimer();
 }
 
 // y(r, c) = f32(sum_gb partial[gb][r][c]), fp64, blocks ascending (each
@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
     constexpr int KB = COLS == 4 ? 8 : (COLS == 2 ? 16 : 32);
     V v[KB];
 #pragma unroll
-    for (int k = 0; k < KB; ++k) v[k] = __ldcg(src + min(k, total - 1) * stride);
+    for (int k = 0; k < KB; ++k)
+        if (k < total) v[k] = __ldcg(src + k * stride);  // (no loads past the last block: C4 b = 2 -0.8 us)
     double y[COLS];
 #pragma unroll
     for (int c = 0; c < COLS; ++c) y[c] = 0.0;
@@ -305,7 +306,8 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
         V nv[KB];
         if (more) {
 #pragma unroll
-            for (int k = 0; k < KB; ++k) nv[k] = __ldcg(src + min(q0 + KB + k, total - 1) * stride);
+            for (int k = 0; k < KB; ++k)
+                if (q0 + KB + k < total) nv[k] = __ldcg(src + (q0 + KB + k) * stride);
         }
 #pragma unroll
         for (int k = 0; k < KB; ++k) {
@@ -347,7 +349,7 @@ constexpr size_t kSmemCap = 227 * 1024;
 #endif
 constexpr size_t kMinStages = BQG_FAST_MINR;  // ring depth the stage size is chosen for
 size_t lut_bytes(int mu, int bt) { return (size_t(1) << mu) * (bt == 1 ? 64 : 32 * bt) * 4; }
-size_t smem_tail(int mu, int bt) { return 2 * kMaxStages * sizeof(uint64_t) + size_t(32) * mu * bt * 4; }
+size_t smem_tail(int mu, int bt) { return 2 * kMaxStages * sizeof(uint64_t) + size_t(xs_words(mu, bt)) * 4; }
 size_t fast_smem_bytes(const FastPlan& pl, int mu, int bt, int beta) {
     return lut_bytes(mu, bt) + size_t(pl.R) * pl.tps * beta * 1024 + smem_tail(mu, bt);
 }
@@ -388,6 +390,7 @@ cudaError_t launch_mu_bt(const QueryParams& p, const FastPlan& plan, bool pdl, c
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, plan);
     if (e != cudaSuccess) return e;
+    if (p.debug & (1 << 20)) return cudaSuccess;  // profiling: no finaliser (y not written)
     // finaliser: always PDL-chained to the fused kernel
     cudaLaunchConfig_t f = {};
     // one thread per (column tile, row), or per (column tile, row, column)

@@ -728,6 +728,24 @@ bool tex_stream_applies(long long m, int G, int beta) {
     return bytes / 16 + 2 * (kWinAlign / 16) <= max_texels(dev);
 }
 
+cudaError_t zero_counters_once(void* ws, int dev, cudaStream_t stream) {
+    // The counters must be zero before a workspace's first launch (the C ABI
+    // documents it; the library's own allocators zero-fill).  As a safety net
+    // a workspace not seen before is zeroed on the stream -- inside a graph
+    // capture the memset becomes a graph node.
+    static std::mutex mu;
+    static std::unordered_map<uintptr_t, int> seen;
+    const uintptr_t key = reinterpret_cast<uintptr_t>(ws) ^ (static_cast<uintptr_t>(dev) << 56);
+    std::lock_guard<std::mutex> lk(mu);
+    if (seen.count(key)) return cudaSuccess;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    const cudaError_t e = cudaMemsetAsync(ws, 0, kTexCounterBytes, stream);
+    if (e != cudaSuccess) return e;
+    if (cs == cudaStreamCaptureStatusNone) seen.emplace(key, 1);
+    return cudaSuccess;
+}
+
 cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
                                float* ws, bool pdl, cudaStream_t stream, const float* local_base,
                                float* const* peer_base, int npeer) {
@@ -746,23 +764,8 @@ cudaError_t launch_biqgemm_tex(const StreamCall* calls, int count, long long x_r
     A.NB = (G + 31) / 32;
     A.MT = (m + 31) / 32;
     A.cnt = reinterpret_cast<unsigned*>(ws);  // kTexCounterBytes, then the partials
-    {
-        // The counters must be zero before a workspace's first launch (the
-        // C ABI documents it; the library's own allocators zero-fill).  As a
-        // safety net a workspace not seen before is zeroed on the stream --
-        // inside a graph capture the memset becomes a graph node.
-        static std::mutex mu;
-        static std::unordered_map<uintptr_t, int> seen;
-        const uintptr_t key = reinterpret_cast<uintptr_t>(ws) ^ (static_cast<uintptr_t>(dev) << 56);
-        std::lock_guard<std::mutex> lk(mu);
-        if (!seen.count(key)) {
-            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-            cudaStreamIsCapturing(stream, &cs);
-            e = cudaMemsetAsync(ws, 0, kTexCounterBytes, stream);
-            if (e != cudaSuccess) return e;
-            if (cs == cudaStreamCaptureStatusNone) seen.emplace(key, 1);
-        }
-    }
+    e = zero_counters_once(ws, dev, stream);
+    if (e != cudaSuccess) return e;
     A.partial = ws + kTexCounterBytes / sizeof(float);
     static const bool verbose = getenv("BQG_TEX_VERBOSE") != nullptr;
     const size_t key_bytes = static_cast<size_t>(A.NB) * A.MT * beta * 1024;

@@ -33,6 +33,10 @@ constexpr int kStreamMaxGroup = 512;  // calls per launch (kernel-parameter arra
 // workspace (a layer handle's, the grouped host pipeline's) never clobber the
 // counters.
 constexpr size_t kTexCounterBytes = kStreamMaxGroup * sizeof(unsigned);
+// Zero the counters of a workspace the library has not seen before (on
+// `stream`; a graph node under capture) -- a safety net behind the C ABI's
+// zero-at-allocation rule.
+cudaError_t zero_counters_once(void* ws, int dev, cudaStream_t stream);
 
 // Fused all-gather (biqgemm_tex.cu's finaliser, the two-kernel form's
 // finalize_kernel): every y row is also stored at the same offset from a

@@ -167,6 +167,20 @@ __device__ __forceinline__ void stage_x_tile(float* xs, const float* __restrict_
     }
 }
 
+// The staged x tile in shared memory: lane l's MU x BT inputs (its group's
+// rows, BT columns) at xs + l*XS.  XS = BT * (MU rounded up to odd): with an
+// odd number of BT-vectors per lane the build's per-lane vector reads hit
+// distinct banks (an unpadded 32*BT-word stride put all 32 lanes on one bank
+// group: 32-way conflicts, ~1.6 us of a 2.2 us BT = 4 build).
+__host__ __device__ constexpr int xs_stride(int mu, int bt) { return bt * (mu % 2 == 0 ? mu + 1 : mu); }
+__host__ __device__ constexpr int xs_words(int mu, int bt) { return 32 * xs_stride(mu, bt); }
+// Slot of element idx = (block row rl) * BT + column of the unpadded tile.
+template <int MU, int BT>
+__device__ __forceinline__ int xs_slot(int idx) {
+    const int rl = idx / BT, c = idx - (idx / BT) * BT;
+    return (rl / MU) * xs_stride(MU, BT) + (rl - (rl / MU) * MU) * BT + c;
+}
+
 // build_bank_owned_tables with x read from the staged shared-memory tile
 // (identical arithmetic and order; lane l owns group gb*32 + l).
 template <int MU, int NW, int BT, int KROW = 32 * BT>
@@ -176,10 +190,23 @@ __device__ __forceinline__ void build_bank_owned_tables_smem(float* lut, const f
     constexpr int TABLE = 1 << MU;
     if (warp >= NCH) return;
     float xv[MU][BT];
+    const float* xl = xs + lane * xs_stride(MU, BT);  // 16-byte aligned for BT = 4, 8 for BT = 2
 #pragma unroll
-    for (int t = 0; t < MU; ++t)
-#pragma unroll
-        for (int c = 0; c < BT; ++c) xv[t][c] = xs[(lane * MU + t) * BT + c];
+    for (int t = 0; t < MU; ++t) {
+        if constexpr (BT == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(xl + t * 4);
+            xv[t][0] = v.x;
+            xv[t][1] = v.y;
+            xv[t][2] = v.z;
+            xv[t][3] = v.w;
+        } else if constexpr (BT == 2) {
+            const float2 v = *reinterpret_cast<const float2*>(xl + t * 2);
+            xv[t][0] = v.x;
+            xv[t][1] = v.y;
+        } else {
+            xv[t][0] = xl[t];
+        }
+    }
     float low[1 << L][BT];
 #pragma unroll
     for (int c = 0; c < BT; ++c) {

@@ -1,6 +1,6 @@
 """Per-CTA timeline of the fast kernel (BQG_DEBUG_FLAGS=2).
-Slots: 0 start, 1 after griddepcontrol.wait, 2 LUT built, 3 first key stage
-landed, 4 query done, 5 smid, 6/7 clock64 start/end."""
+Slots: 0 start, 1 after griddepcontrol.wait, 2 first LUT built, 3 first key
+stage landed, 4 query done, 5 smid, 6/7 last segment start / LUT built."""
 import ctypes as C
 import os
 import sys
@@ -50,5 +50,12 @@ if CLUSTER and int(os.environ["BQG_DEBUG_FLAGS"]) & 1024:
 if CLUSTER:
     rows += [("bar_init", t[:, 14] - t0), ("syncthreads", t[:, 15] - t0), ("tma_issue0", t[:, 13] - t0),
              ("pre_pdlwait", t[:, 12] - t0)]
+if not CLUSTER:
+    two = t[:, 6] > 0
+    print(f"CTAs with a second segment: {int(two.sum())}")
+    if two.any():
+        rows += [("seg2_start", t[two, 6] - t0), ("seg2_built", t[two, 7] - t0),
+                 ("d seg2 build", t[two, 7] - t[two, 6]), ("d seg1 query", t[two, 6] - t[two, 2]),
+                 ("d seg2 query", t[two, 4] - t[two, 7])]
 for name, v in rows:
     print(f"{name:12s} min {v.min():7d} med {int(np.median(v)):7d} max {v.max():7d} ns")
