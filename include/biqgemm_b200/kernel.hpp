@@ -5,10 +5,11 @@
 // biqgemm), same validation and exceptions (kernel.hpp:127-143), same
 // accumulate-into-stats contract (kernel.hpp:197-202).  The multiply runs on
 // the B200:
-//   - T = float, mu <= 8 : the fast path (fused LUT build / gather / alpha
-//     epilogue, fp32 tables; ||y - y_ref||_F / ||y_ref||_F <= 1e-5);
-//   - T = double, mu > 8, or KernelOptions::exact : the exact path (fp64
-//     tables and accumulation in the reference's order: bit-identical y).
+//   - T = float : the fast path (fused LUT build / gather / alpha epilogue,
+//     fp32 tables; ||y - y_ref||_F / ||y_ref||_F <= 1e-5); mu > 8 runs the
+//     same kernels on the sign bits re-keyed to mu = 8 (bqg_rekey_mu8);
+//   - T = double, or KernelOptions::exact : the exact path (fp64 tables and
+//     accumulation in the reference's order: bit-identical y).
 // A PackedLinear (and a KeyMatrix used with biqgemm_plane) uploads itself to
 // the device on first use and keeps the device copy; call reset_device()
 // after mutating keys/alphas in place.  KernelOptions::builder = Naive runs
@@ -55,7 +56,7 @@ struct OpCounters {
     }
 };
 
-// Phase split on the GPU (kernel.hpp:41-46).  Exact path (double, mu > 8,
+// Phase split on the GPU (kernel.hpp:41-46).  Exact path (double,
 // KernelOptions::exact, or builder = Naive): build = the LUT kernels, query =
 // the lookup kernels, replace = setup + alpha epilogue + x upload + y
 // download -- the reference's split.  Fast path: the LUT build runs inside the

@@ -125,6 +125,19 @@ int bqg_pack_keys(const uint32_t* d_plane, size_t m, size_t n, unsigned mu, void
 int bqg_tile_keys(const uint8_t* d_keys, size_t m, size_t n, unsigned beta, unsigned mu,
                   uint8_t* d_tiled, void* stream);
 
+/* mu > 8 on the fast path: the sign bits of mu-bit keys (beta x m x G, u16
+ * for mu > 8, u8 otherwise) re-keyed as mu = 8 keys over
+ * bqg_rekey_mu8_columns(n, mu) = 8*ceil(G*mu/8) columns (beta x m x that/8
+ * bytes, row-major; bits past G*mu are 0, like the keys' own pad bits).
+ * y = sum_i alpha_i * W_i x does not depend on the grouping, so these keys
+ * (then bqg_tile_keys with mu = 8 and n = that column count) run the mu <= 8
+ * kernels -- fp32 tables, within the fast path's contract of the reference's
+ * mu result; the exact path keeps the mu-bit keys and stays bit-identical.
+ * The key stream shrinks too: 1 bit per weight instead of 16/mu. */
+size_t bqg_rekey_mu8_columns(size_t n, unsigned mu);
+int bqg_rekey_mu8(const void* d_keys, size_t m, size_t n, unsigned beta, unsigned mu, uint8_t* d_keys8,
+                  void* stream);
+
 /* build_lut_block (lut.hpp:109-154) for groups [g0, g0+count) of x
  * (x_rows x b), in the reference's LutBlock layout (lut.hpp:90-97).
  *   _f32: the fast path's bank-owned shared-memory builder (mu <= 8),
@@ -274,14 +287,22 @@ void bqg_layer_destroy(bqg_layer* layer);
 int bqg_layer_shape(const bqg_layer* layer, size_t* m, size_t* n, unsigned* beta, unsigned* mu);
 /* Download keys (row-major, u8/u16) and alpha; plane words too if non-NULL. */
 int bqg_layer_export(const bqg_layer* layer, void* h_keys, float* h_alpha, uint32_t* h_planes);
-/* Device views (for device-resident timing and the sharded driver). */
+/* The fast path's view of a layer: (n, mu) for mu <= 8; for mu > 8 the
+ * re-keyed (bqg_rekey_mu8_columns(n, mu), 8) -- the shape its tiled keys
+ * have.  A call whose x has at most 8*ceil(n/8) rows runs with that many
+ * columns (a prefix of the tiled layout: group blocks are its outer index),
+ * so a mu > 8 layer of n columns takes the forms a mu = 8 layer takes. */
+int bqg_layer_fast_shape(const bqg_layer* layer, size_t* n_fast, unsigned* mu_fast);
+/* Device views (for device-resident timing and the sharded driver); the
+ * tiled keys are in the fast view (bqg_layer_fast_shape). */
 const uint8_t* bqg_layer_device_tiled_keys(const bqg_layer* layer);
 const void* bqg_layer_device_keys(const bqg_layer* layer);
 const float* bqg_layer_device_alpha(const bqg_layer* layer);
 
 /* biqgemm(model, x) with HOST x (x_rows x b) and HOST y (m x b): H2D of x,
  * the fused kernel, D2H of y, synchronised before return -- the reference
- * call's contract.  exact selects the path: BQG_FORWARD_FAST (0), or the
+ * call's contract.  exact selects the path: BQG_FORWARD_FAST (0; any mu,
+ * mu > 8 through the re-keyed mu = 8 kernels), or the
  * exact (fp64, bit-identical) path with the reference's Dp builder
  * (BQG_FORWARD_EXACT, any nonzero value) or its Naive builder
  * (BQG_FORWARD_EXACT_NAIVE; KernelOptions::builder, kernel.hpp:51,158).

@@ -145,6 +145,9 @@ SIGNATURES = {
     "bqg_biqgemm_sharded_p2p_workspace_bytes": (sz, [sz, sz, sz, u32, u32, i32]),
     "bqg_biqgemm_sharded_p2p_f32": (i32, [vp, vp, vp, sz, vp, sz, sz, sz, u32, u32, i32, i32, P(Collectives), vp,
                                           sz, vp]),
+    "bqg_rekey_mu8_columns": (sz, [sz, u32]),
+    "bqg_rekey_mu8": (i32, [vp, sz, sz, u32, u32, vp, vp]),
+    "bqg_layer_fast_shape": (i32, [vp, P(sz), P(u32)]),
     "bqg_ipc_get_handle": (i32, [vp, vp, P(sz)]),
     "bqg_ipc_open_handle": (i32, [vp, sz, P(vp)]),
     "bqg_ipc_close_handle": (i32, [vp]),

@@ -187,6 +187,27 @@ extern "C" size_t bqg_tiled_key_bytes(size_t m, size_t n, unsigned beta, unsigne
     return ((G + 31) / 32) * beta * ((m + 31) / 32) * 1024;
 }
 
+extern "C" size_t bqg_rekey_mu8_columns(size_t n, unsigned mu) {
+    if (mu < 1 || mu > 16 || n == 0) return 0;
+    return 8 * ((groups_of(n, mu) * mu + 7) / 8);
+}
+
+extern "C" int bqg_rekey_mu8(const void* d_keys, size_t m, size_t n, unsigned beta, unsigned mu, uint8_t* d_keys8,
+                             void* stream) {
+    int s = check_mu(mu, "rekey_mu8");
+    if (s) return s;
+    s = check_dims(m, n, "rekey_mu8");
+    if (s) return s;
+    if (beta == 0 || !d_keys || !d_keys8) return set_err(BQG_ERR_INVALID_ARGUMENT, "rekey_mu8: bad argument");
+    BQG_NEED_DEVICE();
+    const size_t n8 = bqg_rekey_mu8_columns(n, mu);
+    cudaError_t e = bqg::launch_rekey_mu8(d_keys, static_cast<long long>(beta) * static_cast<long long>(m),
+                                          static_cast<long long>(groups_of(n, mu)), static_cast<int>(mu),
+                                          static_cast<long long>(n8 / 8), d_keys8, as_stream(stream));
+    if (e != cudaSuccess) return cuda_err(e, "rekey_mu8 kernel");
+    return BQG_OK;
+}
+
 // ---- BQGM (model_io.cpp:65-141) ----
 
 namespace {
@@ -703,11 +724,17 @@ struct bqg_layer {
     uint64_t uid = 0;  // process-unique (a new layer at a freed layer's address is a different layer)
     size_t m = 0, n = 0, G = 0;
     unsigned beta = 0, mu = 0;
+    // The fast path's view: mu <= 8 -> (n, mu); mu > 8 -> the sign bits
+    // re-keyed to mu = 8 over fn = bqg_rekey_mu8_columns(n, mu) columns (the
+    // fast kernels' u8 keys and shared-memory tables; y within the fp32
+    // contract of the reference's mu, the exact path stays bit-identical).
+    size_t fn = 0;
+    unsigned fmu = 0;
     bool plane_mode = false;
     cudaStream_t stream = nullptr;
     uint32_t* d_planes = nullptr;  // only when created from weights
     void* d_keys = nullptr;        // row-major u8/u16
-    uint8_t* d_tiled = nullptr;    // mu <= 8
+    uint8_t* d_tiled = nullptr;    // tiled u8 keys of the fast view (fn, fmu)
     float* d_alpha = nullptr;
     // forward scratch (grown on demand)
     void* d_ws = nullptr;
@@ -774,10 +801,13 @@ int layer_alloc(size_t m, size_t n, unsigned beta, unsigned mu, bool plane_mode,
     L->beta = beta;
     L->mu = mu;
     L->G = groups_of(n, mu);
+    L->fn = mu <= 8 ? n : bqg_rekey_mu8_columns(n, mu);
+    L->fmu = mu <= 8 ? mu : 8;
     L->plane_mode = plane_mode;
     cudaError_t e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&L->d_keys, L->key_bytes_per_plane() * beta);
-    if (e == cudaSuccess && mu <= 8) e = cudaMalloc(reinterpret_cast<void**>(&L->d_tiled), bqg_tiled_key_bytes(m, n, beta, mu));
+    if (e == cudaSuccess)
+        e = cudaMalloc(reinterpret_cast<void**>(&L->d_tiled), bqg_tiled_key_bytes(m, L->fn, beta, L->fmu));
     if (e == cudaSuccess && !plane_mode) e = cudaMalloc(reinterpret_cast<void**>(&L->d_alpha), sizeof(float) * beta * m);
     for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&L->ev[i]);
     if (e != cudaSuccess) {
@@ -794,6 +824,20 @@ int layer_finish_tiling(bqg_layer* L) {
                                               static_cast<long long>(L->G), static_cast<int>(L->beta), L->d_tiled,
                                               L->stream);
         if (e != cudaSuccess) return cuda_err(e, "tile_keys kernel");
+    } else {
+        // mu > 8: the same sign bits as mu = 8 keys, then the fast path's tiling
+        uint8_t* k8 = nullptr;
+        const size_t g8 = L->fn / 8;
+        BQG_CUDA(cudaMalloc(reinterpret_cast<void**>(&k8), size_t(L->beta) * L->m * g8));
+        int s = bqg_rekey_mu8(L->d_keys, L->m, L->n, L->beta, L->mu, k8, L->stream);
+        cudaError_t e = s ? cudaSuccess
+                          : bqg::launch_tile_keys(k8, static_cast<long long>(L->m), static_cast<long long>(g8),
+                                                  static_cast<int>(L->beta), L->d_tiled, L->stream);
+        cudaError_t e2 = cudaStreamSynchronize(L->stream);
+        cudaFree(k8);
+        if (s) return s;
+        if (e != cudaSuccess) return cuda_err(e, "tile_keys kernel");
+        if (e2 != cudaSuccess) return cuda_err(e2, "rekey");
     }
     BQG_CUDA(cudaStreamSynchronize(L->stream));
     return BQG_OK;
@@ -954,11 +998,29 @@ extern "C" int bqg_layer_export(const bqg_layer* L, void* h_keys, float* h_alpha
     return BQG_OK;
 }
 
+extern "C" int bqg_layer_fast_shape(const bqg_layer* L, size_t* n_fast, unsigned* mu_fast) {
+    if (!L) return set_err(BQG_ERR_INVALID_ARGUMENT, "layer: null");
+    if (n_fast) *n_fast = L->fn;
+    if (mu_fast) *mu_fast = L->fmu;
+    return BQG_OK;
+}
 extern "C" const uint8_t* bqg_layer_device_tiled_keys(const bqg_layer* L) { return L ? L->d_tiled : nullptr; }
 extern "C" const void* bqg_layer_device_keys(const bqg_layer* L) { return L ? L->d_keys : nullptr; }
 extern "C" const float* bqg_layer_device_alpha(const bqg_layer* L) { return L ? L->d_alpha : nullptr; }
 
 namespace {
+
+// Columns of the fast view a call with x_rows input rows needs: mu <= 8 ->
+// n; mu > 8 -> 8*ceil(n/8) when x reaches no further (its groups are a prefix
+// of the re-keyed tiling: blocks are the layout's outer index), else the
+// whole re-keyed width (x rows past n meet the pad bits' sign).  A call
+// covering n keeps the group blocks a mu = 8 layer of n columns has (C2:
+// 16, the latency form's shape) instead of one more nearly empty block.
+size_t fast_columns(const bqg_layer* L, size_t x_rows) {
+    if (L->mu <= 8) return L->n;
+    const size_t n8 = 8 * ((L->n + 7) / 8);
+    return x_rows <= n8 ? n8 : L->fn;
+}
 
 // exact: BQG_FORWARD_FAST (0), BQG_FORWARD_EXACT (fp64 DP tables) or
 // BQG_FORWARD_EXACT_NAIVE (fp64 naive tables: KernelOptions::builder = Naive,
@@ -966,7 +1028,7 @@ namespace {
 // counters and build/query/replace split; it synchronises the stream.
 int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float* d_y, int exact, int pdl,
                   cudaStream_t st, bqg_kernel_stats* xstats = nullptr) {
-    if (exact || L->mu > 8) {
+    if (exact) {
         const size_t need = bqg_biqgemm_exact_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
         if (need > L->ws_exact_bytes) ++L->buf_gen;
         int s = grow(L->d_ws_exact, L->ws_exact_bytes, need, st);
@@ -975,13 +1037,15 @@ int layer_forward(bqg_layer* L, const float* d_x, size_t x_rows, size_t b, float
                                          exact == BQG_FORWARD_EXACT_NAIVE ? BQG_LUT_NAIVE : BQG_LUT_DP,
                                          L->d_ws_exact, L->ws_exact_bytes, xstats, st);
     }
-    const size_t need = bqg_biqgemm_workspace_bytes(L->m, L->n, b, L->beta, L->mu);
+    // the fast view (mu > 8: the re-keyed mu = 8 tiles over fn >= G*mu columns)
+    const size_t fn = fast_columns(L, x_rows);
+    const size_t need = bqg_biqgemm_workspace_bytes(L->m, fn, b, L->beta, L->fmu);
     if (need > L->ws_bytes) {
         ++L->buf_gen;
         int s = grow(L->d_ws, L->ws_bytes, need, st);
         if (s) return s;
     }
-    return bqg_biqgemm_f32(L->d_tiled, L->d_alpha, d_x, x_rows, d_y, L->m, L->n, b, L->beta, L->mu, L->d_ws,
+    return bqg_biqgemm_f32(L->d_tiled, L->d_alpha, d_x, x_rows, d_y, L->m, fn, b, L->beta, L->fmu, L->d_ws,
                            L->ws_bytes, pdl, st);
 }
 
@@ -1098,7 +1162,7 @@ extern "C" int bqg_layer_forward_host(bqg_layer* L, const float* h_x, size_t x_r
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[0], st));
     BQG_CUDA(cudaMemcpyAsync(L->d_x, xpin ? h_x : L->h_x_pin, xbytes, cudaMemcpyHostToDevice, st));
     if (stats) BQG_CUDA(cudaEventRecord(L->ev[1], st));
-    const bool exact_path = exact || L->mu > 8;
+    const bool exact_path = exact != 0;
     bqg_kernel_stats xs{};
     s = layer_forward(L, L->d_x, x_rows, b, L->d_y, exact, 0, st, exact_path ? &xs : nullptr);
     if (s) return s;
@@ -1189,7 +1253,7 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
     }
     int s = check_x(x_rows, b, L0->n, L0->mu, "biqgemm");
     if (s) return s;
-    if (exact || L0->mu > 8) {
+    if (exact) {
         for (size_t i = 0; i < count; ++i) {
             s = bqg_layer_forward_host(layers[i], h_x + i * x_rows * b, x_rows, b, h_y + i * L0->m * b, exact, stats);
             if (s) return s;
@@ -1282,7 +1346,9 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
         G.chunk_ev.push_back(e);
     }
     s = grow(G.d_ws, G.ws_cap,
-             bqg_biqgemm_grouped_workspace_bytes(L0->m, L0->n, b, L0->beta, L0->mu, std::min(count, kSub)), G.stream);
+             bqg_biqgemm_grouped_workspace_bytes(L0->m, fast_columns(L0, x_rows), b, L0->beta, L0->fmu,
+                                                 std::min(count, kSub)),
+             G.stream);
     if (s) return s;
     std::vector<bqg_call> calls(count);
     for (size_t i = 0; i < count; ++i) calls[i] = {layers[i]->d_tiled, layers[i]->d_alpha, G.d_x + i * xs, G.d_y + i * ys};
@@ -1308,7 +1374,8 @@ extern "C" int bqg_layers_forward_host(bqg_layer* const* layers, size_t count, c
             cudaEvent_t h2d = G.chunk_ev[2 * k], done = G.chunk_ev[2 * k + 1];
             BQG_CUDA(cudaStreamWaitEvent(st, h2d, 0));
             if (stats && k == 0) BQG_CUDA(cudaEventRecord(G.ev[1], st));
-            const int rc = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, L0->n, b, L0->beta, L0->mu,
+            const int rc = bqg_biqgemm_grouped_f32(calls.data() + i0, cnt, x_rows, L0->m, fast_columns(L0, x_rows), b,
+                                                   L0->beta, L0->fmu,
                                                    G.d_ws, G.ws_cap, k > 0 ? 1 : 0, st);
             if (rc) return rc;
             BQG_CUDA(cudaEventRecord(done, st));

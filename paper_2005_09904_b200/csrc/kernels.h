@@ -111,6 +111,10 @@ cudaError_t launch_quantize_greedy(const T* w, long long m, long long n, int bet
                                    cudaStream_t stream);
 cudaError_t launch_pack_keys(const uint32_t* plane, long long m, long long n, int mu, void* keys,
                              cudaStream_t stream);
+// keys (rows x groups, mu-bit, u8 / u16) -> the same sign bits as mu = 8 keys
+// (rows x groups8 bytes, groups8 >= ceil(groups*mu / 8)); rows = beta*m.
+cudaError_t launch_rekey_mu8(const void* keys, long long rows, long long groups, int mu, long long groups8,
+                             uint8_t* out, cudaStream_t stream);
 cudaError_t launch_tile_keys(const uint8_t* keys, long long m, long long groups, int beta,
                              uint8_t* tiled, cudaStream_t stream);
 

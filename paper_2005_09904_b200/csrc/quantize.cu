@@ -134,7 +134,40 @@ __global__ void tile_keys_kernel(const uint8_t* __restrict__ keys, long long m, 
     out[idx] = v;
 }
 
+// Re-key mu-bit keys (u8 for mu <= 8, u16 above) to mu = 8: byte g8 of row r
+// holds the sign bits of weights 8*g8 .. 8*g8+7 (bit t = weight 8*g8 + t,
+// packing.hpp:61-81's order), i.e. bit (8*g8 + t) % mu of key (8*g8 + t) / mu;
+// bits past the G*mu bits of a row are 0 -- exactly the pad bits the keys
+// carry past n, so every x row the mu-keys accept meets the same sign.
+template <typename K>
+__global__ void rekey_mu8_kernel(const K* __restrict__ keys, long long rows, long long groups, int mu,
+                                 long long groups8, uint8_t* __restrict__ out) {
+    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= rows * groups8) return;
+    const long long r = idx / groups8, g8 = idx - r * groups8;
+    const K* kr = keys + r * groups;
+    unsigned v = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const long long w = g8 * 8 + t, g = w / mu;
+        if (g < groups) v |= ((static_cast<unsigned>(kr[g]) >> static_cast<int>(w - g * mu)) & 1u) << t;
+    }
+    out[idx] = static_cast<uint8_t>(v);
+}
+
 }  // namespace
+
+cudaError_t launch_rekey_mu8(const void* keys, long long rows, long long groups, int mu, long long groups8,
+                             uint8_t* out, cudaStream_t stream) {
+    const long long total = rows * groups8;
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+    if (mu <= 8)
+        rekey_mu8_kernel<uint8_t><<<grid, 256, 0, stream>>>(static_cast<const uint8_t*>(keys), rows, groups, mu, groups8, out);
+    else
+        rekey_mu8_kernel<uint16_t><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(keys), rows, groups, mu, groups8,
+                                                            out);
+    return cudaGetLastError();
+}
 
 template <typename T>
 cudaError_t launch_quantize_greedy(const T* w, long long m, long long n, int beta,

@@ -161,12 +161,10 @@ def test_fixtures_fast_and_exact(bq, cuda):
         layer = bq.PackedLinear.from_keys(keys, c["alpha"], n, mu)
         y_exact = layer.forward(x, exact=True)
         assert np.array_equal(y_exact, c["y"]), f"exact path not bit-identical (mu={mu})"
-        if mu <= 8:
-            assert_close(layer.forward(x), c["y"])
+        assert_close(layer.forward(x), c["y"])  # mu > 8: the re-keyed mu = 8 fast path
         plane = bq.PackedLinear.from_keys(keys[:1], None, n, mu)
         assert np.array_equal(plane.forward(x, exact=True), c["yplane"])
-        if mu <= 8:
-            assert_close(plane.forward(x), c["yplane"])
+        assert_close(plane.forward(x), c["yplane"])
         layer.close()
         plane.close()
 
@@ -256,7 +254,50 @@ def test_bqgm_load_forward(bq, ref, cuda):
     layer12 = bq.PackedLinear.load(ref.save_bqgm(w, 2, 12))
     _, _, _, _, _, k12, a12 = ref.load_bqgm(ref.save_bqgm(w, 2, 12))
     y12, _ = ref.biqgemm(k12, a12, 500, 12, x)
-    assert np.array_equal(layer12.forward(x), y12)  # mu > 8 -> exact path
+    assert np.array_equal(layer12.forward(x, exact=True), y12)
+    assert_close(layer12.forward(x), y12)  # the re-keyed mu = 8 fast path
+
+
+@pytest.mark.parametrize("m,n,beta,mu", [(300, 500, 2, 12), (1000, 777, 3, 10), (64, 4096, 1, 9), (96, 1000, 2, 16),
+                                         (4096, 4096, 3, 10), (33, 13, 2, 11)])
+def test_large_mu_fast_path_rekeyed(bq, port, cuda, m, n, beta, mu):
+    """mu > 8 on the fast path: the sign bits re-keyed to mu = 8 over
+    8*ceil(G*mu/8) columns run the mu <= 8 kernels.  y within the fp32
+    contract of the reference's mu-bit result for every x length the mu-keys
+    accept -- x shorter than n, x = n, and x = G*mu rows (past n: the pad
+    bits' sign); the re-keyed bytes are the mu = 8 packing of the same
+    bits."""
+    import ctypes as C
+
+    import torch
+
+    w = bq.random_uniform(m, n, 11 + mu)
+    layer = bq.PackedLinear.from_weights(w, beta, mu)
+    keys, alpha = layer.export()
+    G = (n + mu - 1) // mu
+    n8, mu8 = C.c_size_t(), C.c_uint()
+    bq.check(bq.lib.bqg_layer_fast_shape(layer._h, C.byref(n8), C.byref(mu8)))
+    assert (n8.value, mu8.value) == (8 * ((G * mu + 7) // 8), 8)
+    # the re-keyed bytes: the same sign bits packed 8 per byte
+    bits = ((keys.astype(np.uint32)[..., None] >> np.arange(mu, dtype=np.uint32)) & 1).reshape(beta, m, G * mu)
+    bits = np.concatenate([bits, np.zeros((beta, m, n8.value - G * mu), np.uint32)], axis=2)
+    want8 = (bits.reshape(beta, m, -1, 8) << np.arange(8, dtype=np.uint32)).sum(-1).astype(np.uint8)
+    kd = torch.from_numpy(keys.view(np.int16) if mu > 8 else keys).cuda()
+    out = torch.empty((beta, m, n8.value // 8), dtype=torch.uint8, device="cuda")
+    bq.check(bq.lib.bqg_rekey_mu8(kd.data_ptr(), m, n, beta, mu, out.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want8)
+    for rows, b in ((n, 1), (n, 3), (max(1, n // 2), 2), (G * mu, 1)):
+        x = bq.random_normal(rows, b, 5 + rows)
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x)
+        assert_close(layer.forward(x), y_ref)
+        assert np.array_equal(layer.forward(x, exact=True), layer.forward(x, exact=True))
+    # a group of such layers through the grouped host pipeline == one by one
+    xs = np.stack([bq.random_normal(n, 1, 40 + i) for i in range(6)])
+    yg = bq.layers_forward([layer] * 6, xs)
+    for i in range(6):
+        assert np.array_equal(yg[i], layer.forward(xs[i]))
+    layer.close()
 
 
 def test_stats_counters_and_accumulation(bq, cuda):
