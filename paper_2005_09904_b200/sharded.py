@@ -224,6 +224,10 @@ class ShardedLinear:
         self.bq = bq
         self.layer = shard_layer  # PackedLinear of rows [lo, hi) (None when the rank owns no rows)
         self.m, self.n, self.beta, self.mu = m, n, beta, mu
+        # the kernels' view: mu > 8 layers run the fast path on their sign bits
+        # re-keyed to mu = 8 (bqg_rekey_mu8; the layer's tiled keys) over
+        # 8*ceil(n/8) columns -- x may have up to that many rows
+        self.kn, self.kmu = (n, mu) if mu <= 8 else (8 * ((n + 7) // 8), 8)
         self.rank, self.world = rank, world
         self.plan = ShardPlan.make(m, world)
         self.coll_provider = collectives
@@ -251,7 +255,7 @@ class ShardedLinear:
         if b not in self._ws:
             bq = self.bq
             self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_workspace_bytes(
-                self.m, self.n, b, self.beta, self.mu, self.world)), device=self.device)
+                self.m, self.kn, b, self.beta, self.kmu, self.world)), device=self.device)
         return self._ws[b]
 
     def forward_device(self, x: torch.Tensor, y_gather: torch.Tensor, stream=None) -> torch.Tensor:
@@ -268,7 +272,7 @@ class ShardedLinear:
         alpha = self.layer.device_alpha if self.layer is not None else None
         coll = self.coll_provider.collectives()
         bq.check(bq.lib.bqg_biqgemm_sharded_f32(keys, alpha, x.data_ptr(), x_rows, y_gather.data_ptr(), self.m,
-                                                self.n, b, self.beta, self.mu, self.rank, self.world,
+                                                self.kn, b, self.beta, self.kmu, self.rank, self.world,
                                                 C.byref(coll), ws.ptr(), ws.nbytes, bq._stream(stream)))
         return y_gather[: self.m]
 
@@ -296,6 +300,7 @@ class ShardedGroup:
         self.bq = bq
         self.shards = list(shards)
         self.m, self.n, self.beta, self.mu = s0.m, s0.n, s0.beta, s0.mu
+        self.kn, self.kmu = s0.kn, s0.kmu
         self.rank, self.world, self.plan, self.device = s0.rank, s0.world, s0.plan, s0.device
         self.coll_provider = s0.coll_provider
         self._arr = (bq._capi.ShardCall * len(self.shards))()
@@ -331,12 +336,12 @@ class ShardedGroup:
             self.coll_provider.register(x, y_gather)
         if b not in self._ws:
             self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_workspace_bytes(
-                self.m, self.n, b, self.beta, self.mu, count, self.world)), device=self.device)
+                self.m, self.kn, b, self.beta, self.kmu, count, self.world)), device=self.device)
         ws = self._ws[b]
         coll = self.coll_provider.collectives()
         bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
-            C.cast(self._arr, C.c_void_p), count, x.data_ptr(), x_rows, y_gather.data_ptr(), self.m, self.n, b,
-            self.beta, self.mu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
+            C.cast(self._arr, C.c_void_p), count, x.data_ptr(), x_rows, y_gather.data_ptr(), self.m, self.kn, b,
+            self.beta, self.kmu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
             bq._stream(stream)))
         return self.assemble(y_gather)
 
@@ -413,14 +418,14 @@ class ShardedGroupP2P(ShardedGroup):
             raise ValueError("ShardedGroupP2P: x must be a contiguous float32 tensor on this rank's device")
         if b not in self._ws:
             self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(
-                self.m, self.n, b, self.beta, self.mu, count, self.world)), device=self.device)
+                self.m, self.kn, b, self.beta, self.kmu, count, self.world)), device=self.device)
         ws = self._ws[b]
         if isinstance(self.coll_provider, TorchCollectives):
             self.coll_provider.register(x, y_gather, ws.buf)
         coll = self.coll_provider.collectives()
         bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
             C.cast(self._arr, C.c_void_p), count, x.data_ptr(), x_rows, C.cast(self.peer.ptrs, C.c_void_p), self.m,
-            self.n, b, self.beta, self.mu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
+            self.kn, b, self.beta, self.kmu, self.rank, self.world, C.byref(coll), ws.ptr(), ws.nbytes, 1 if pdl else 0,
             bq._stream(stream)))
         return self.assemble(y_gather)
 
@@ -454,7 +459,7 @@ class ShardedLinearP2P(ShardedLinear):
         if b not in self._ws:
             bq = self.bq
             self._ws[b] = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_p2p_workspace_bytes(
-                self.m, self.n, b, self.beta, self.mu, self.world)), device=self.device)
+                self.m, self.kn, b, self.beta, self.kmu, self.world)), device=self.device)
         return self._ws[b]
 
     def forward_device(self, x: torch.Tensor, y_gather: torch.Tensor = None, stream=None) -> torch.Tensor:
@@ -472,8 +477,8 @@ class ShardedLinearP2P(ShardedLinear):
         alpha = self.layer.device_alpha if self.layer is not None else None
         coll = self.coll_provider.collectives()
         bq.check(bq.lib.bqg_biqgemm_sharded_p2p_f32(keys, alpha, x.data_ptr(), x_rows,
-                                                    C.cast(self.peer.ptrs, C.c_void_p), self.m, self.n, b,
-                                                    self.beta, self.mu, self.rank, self.world, C.byref(coll),
+                                                    C.cast(self.peer.ptrs, C.c_void_p), self.m, self.kn, b,
+                                                    self.beta, self.kmu, self.rank, self.world, C.byref(coll),
                                                     ws.ptr(), ws.nbytes, bq._stream(stream)))
         return y_gather[: self.m]
 

@@ -272,7 +272,7 @@ def test_fused_allgather_peer_stores_single_gpu(cuda, world, m, n, beta, count):
         assert ok, f"rank {rank}: {diff}"
 
 
-def _p2p_single_worker(rank, world, port, m, n, beta, b, out_q):
+def _p2p_single_worker(rank, world, port, m, n, beta, b, out_q, mu=8):
     """One rank of the single-call fused all-gather
     (bqg_biqgemm_sharded_p2p_f32, the north_star C5 decomposition): processes
     on one GPU, gather buffers IPC-mapped, gloo for x and the barrier."""
@@ -285,8 +285,8 @@ def _p2p_single_worker(rank, world, port, m, n, beta, b, out_q):
         from paper_2005_09904_b200.sharded import ShardedLinearP2P, TorchCollectives
 
         w = bq.random_uniform(m, n, 91)
-        sh = ShardedLinearP2P.from_weights(w, beta, 8, rank, world, TorchCollectives(), b=b)
-        full = bq.PackedLinear.from_weights(w, beta, 8)
+        sh = ShardedLinearP2P.from_weights(w, beta, mu, rank, world, TorchCollectives(), b=b)
+        full = bq.PackedLinear.from_weights(w, beta, mu)
         ok, diff = True, 0.0
         for rep in range(2):
             x_h = bq.random_normal(n, b, 92 + rep)
@@ -308,9 +308,10 @@ def _p2p_single_worker(rank, world, port, m, n, beta, b, out_q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,m,n,beta,b", [(2, 4096, 4096, 2, 8), (3, 1000, 777, 2, 5), (2, 3000, 1024, 3, 16),
-                                              (3, 1000, 777, 2, 2), (2, 4096, 4096, 3, 1)])
-def test_fused_allgather_single_call_single_gpu(cuda, world, m, n, beta, b):
+@pytest.mark.parametrize("world,m,n,beta,b,mu", [(2, 4096, 4096, 2, 8, 8), (3, 1000, 777, 2, 5, 8),
+                                                 (2, 3000, 1024, 3, 16, 8), (3, 1000, 777, 2, 2, 8),
+                                                 (2, 4096, 4096, 3, 1, 8), (2, 1000, 1000, 2, 6, 10)])
+def test_fused_allgather_single_call_single_gpu(cuda, world, m, n, beta, b, mu):
     """bqg_biqgemm_sharded_p2p_f32: the two-kernel finaliser stores every y
     value into every rank's gather buffer; each rank's y == the unsharded
     layer's (which takes the same two-kernel form at these shapes; b = 1 takes
@@ -318,7 +319,7 @@ def test_fused_allgather_single_call_single_gpu(cuda, world, m, n, beta, b):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     portn = _free_port()
-    procs = [ctx.Process(target=_p2p_single_worker, args=(r, world, portn, m, n, beta, b, q)) for r in range(world)]
+    procs = [ctx.Process(target=_p2p_single_worker, args=(r, world, portn, m, n, beta, b, q, mu)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
