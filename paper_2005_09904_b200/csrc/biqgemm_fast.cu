@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(128) finalize_kernel(const QueryParams p) {
         for (int c = 0; c < COLS; ++c)
             if (ct * BT + cc * COLS + c < p.b) py[c] = static_cast<float>(y[c]);
     }
+    if (p.npeer > 0) __threadfence_system();  // peer stores performed before the grid completes
 }
 
 #ifndef BQG_FAST_NW

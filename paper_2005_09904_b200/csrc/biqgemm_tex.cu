@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
         // release: the queue is final (the gather warps sleep on barrier 3)
         if (which == 0) named_bar_arrive(3, (kNW + 1) * 32);
         fin_drain(A, fq, tcur, lane);
+        if (A.npeer > 0) __threadfence_system();  // peer stores (other GPUs' memory) performed before the CTA retires
         return;
     }
 
@@ -627,6 +628,7 @@ __global__ void __launch_bounds__(TexGeom<kNW>::threads, 1) biqgemm_tex_kernel(c
     mbar_arrive(&ldone[cur % kNL]);
     named_bar_sync(3, (kNW + 1) * 32);  // the CTA's last tasks are posted: everyone helps finish them
     fin_drain(A, fq, tcur, lane);
+    if (A.npeer > 0) __threadfence_system();  // peer stores (other GPUs' memory) performed before the CTA retires
 }
 
 // Per-device caches (cudaFuncSetAttribute and the SM count are per device).
