@@ -347,12 +347,8 @@ def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
     if world > 1:
         # every rank's gather buffer mapped into every rank (CUDA IPC): the
         # grouped kernel's finaliser stores y rows straight into all of them
-        from paper_2005_09904_b200.sharded import PeerGather
-
-        peer = PeerGather((world, G, R, b), rank, world, device=dev)
-        y_gather = peer.tensor
-    else:
-        y_gather = torch.empty((world, G, R, b), device=dev)
+        peer = peer_gather_or_none(ctx, (world, G, R, b))
+    y_gather = peer.tensor if peer is not None else torch.empty((world, G, R, b), device=dev)
     y_mine = y_gather[rank]
     ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(world * m, n, b, beta, mu, G, world))
                       if world > 1 else int(bq.lib.bqg_biqgemm_grouped_workspace_bytes(m, n, b, beta, mu, G)),
@@ -388,6 +384,11 @@ def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
         buffer (fused all-gather over peer memory) -> a 16-byte barrier."""
         import ctypes as C
 
+        if peer is None:  # no peer mapping: the NCCL all-gather entry
+            bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
+                C.cast(shard_arrays[s], C.c_void_p), G, x_step.data_ptr(), n, y_gather.data_ptr(), world * m, n, b,
+                beta, mu, rank, world, C.byref(coll_struct), ws.ptr(), ws.nbytes, 1 if pdl else 0, stream.cuda_stream))
+            return
         bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
             C.cast(shard_arrays[s], C.c_void_p), G, x_step.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p), world * m, n,
             b, beta, mu, rank, world, C.byref(coll_struct), ws.ptr(), ws.nbytes, 1 if pdl else 0, stream.cuda_stream))
@@ -509,6 +510,8 @@ def run_grouped(ctx, bq, args, cfg, m, n, beta, b, mu):
     if world > 1:
         line["compute_ms_per_step"] = compute_ms / K
         line["collective_ms_per_step"] = (ms - compute_ms) / K
+        line["y_gather"] = ("fused: peer stores into every rank's CUDA-IPC-mapped gather buffer + 16-byte barrier"
+                            if peer is not None else "NCCL all-gather (peer mapping unavailable)")
 
     if world == 1:
         line["latency"] = latency_chain(ctx, bq, tiled, alphas, x_step, y_mine, m, n, beta, mu, b, kb, peak,
@@ -620,11 +623,9 @@ def e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K):
         al0 = torch.from_numpy(alpha).to(dev)
         n_copies = max(2, int(np.ceil(ROTATE_L2 * L2_BYTES / tiled0.numel())) + 1)
         tl = [tiled0] + [tiled0.clone() for _ in range(n_copies - 1)]
-        from paper_2005_09904_b200.sharded import PeerGather
-
         x_dev = torch.empty((G, n, b), device=dev)
-        peer = PeerGather((world, G, m, b), ctx.rank, world, device=dev)
-        y_gather = peer.tensor
+        peer = peer_gather_or_none(ctx, (world, G, m, b))
+        y_gather = peer.tensor if peer is not None else torch.empty((world, G, m, b), device=dev)
         y_host = torch.empty((world, G, m, b), dtype=torch.float32).pin_memory()
         ws = bq.Workspace(int(bq.lib.bqg_biqgemm_grouped_sharded_p2p_workspace_bytes(world * m, n, b, beta, mu, G,
                                                                                      world)), device=dev)
@@ -643,9 +644,15 @@ def e2e_grouped(ctx, bq, layer, keys, alpha, x_h, m, n, beta, mu, b, kb, G, K):
         def one(s):
             if ctx.rank == 0:
                 x_dev.copy_(x_pin, non_blocking=True)
-            bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
-                C.cast(arrays[s % 8], C.c_void_p), G, x_dev.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p), world * m,
-                n, b, beta, mu, ctx.rank, world, C.byref(cs), ws.ptr(), ws.nbytes, 0, stream.cuda_stream))
+            if peer is None:
+                bq.check(bq.lib.bqg_biqgemm_grouped_sharded_f32(
+                    C.cast(arrays[s % 8], C.c_void_p), G, x_dev.data_ptr(), n, y_gather.data_ptr(), world * m, n, b,
+                    beta, mu, ctx.rank, world, C.byref(cs), ws.ptr(), ws.nbytes, 0, stream.cuda_stream))
+            else:
+                bq.check(bq.lib.bqg_biqgemm_grouped_sharded_p2p_f32(
+                    C.cast(arrays[s % 8], C.c_void_p), G, x_dev.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p),
+                    world * m, n, b, beta, mu, ctx.rank, world, C.byref(cs), ws.ptr(), ws.nbytes, 0,
+                    stream.cuda_stream))
             if ctx.rank == 0:
                 y_host.copy_(y_gather, non_blocking=True)
             stream.synchronize()
@@ -761,6 +768,33 @@ def run_single(ctx, bq, args, cfg, m, n, beta, b, mu):
 # ---------------------------------------------------- C5 strong scaling
 
 
+def peer_gather_or_none(ctx, shape):
+    """Every rank's gather buffer mapped into every rank (CUDA IPC) for the
+    fused all-gather, or None on EVERY rank when any rank cannot map a peer
+    (the sharded entries then gather y with the NCCL all-gather instead; the
+    decision is collective so all ranks take the same collective path)."""
+    from paper_2005_09904_b200.sharded import PeerGather
+
+    torch = ctx.torch
+    peer, ok = None, 1
+    try:
+        if os.environ.get("BQG_BENCH_NO_P2P") == "1":  # A/B: the NCCL all-gather entries
+            raise RuntimeError("BQG_BENCH_NO_P2P=1")
+        peer = PeerGather(shape, ctx.rank, ctx.world, device=ctx.dev)
+    except Exception as e:  # noqa: BLE001 -- reported, and the NCCL path runs instead
+        print(f"[bench] rank {ctx.rank}: fused all-gather unavailable ({e}); using the NCCL all-gather",
+              file=sys.stderr)
+        ok = 0
+    if ctx.world > 1:
+        t = torch.tensor([ok], device=ctx.dev, dtype=torch.int32)
+        ctx.dist.all_reduce(t, op=ctx.dist.ReduceOp.MIN)
+        ok = int(t.item())
+    if not ok and peer is not None:
+        peer.close()
+        peer = None
+    return peer
+
+
 def c5_inputs(bq):
     """C5 (BASELINE configs[4]): 65536x8192, q2, mu 8, b 8.  Keys and alpha are
     seeded random (identical on every rank), x from the bench_cli generator."""
@@ -787,17 +821,25 @@ def c5_time(ctx, bq, keys, alpha, x, rank, world, coll, K, W):
     t0 = bq.tile_keys(torch.from_numpy(np.ascontiguousarray(keys[:, lo:hi])).to(dev), n, mu)
     a0 = torch.from_numpy(np.ascontiguousarray(alpha[:, lo:hi])).to(dev)
     tiled, alphas, copies = rotating_copies(ctx, t0, a0)
-    from paper_2005_09904_b200.sharded import PeerGather
-
     x_dev = torch.from_numpy(x).to(dev)
-    peer = PeerGather((world * R, b), rank, world, device=dev)  # every rank's gather buffer, IPC-mapped
-    y_gather = peer.tensor
+    if world == ctx.world:  # every rank's gather buffer, IPC-mapped (or the NCCL all-gather)
+        peer = peer_gather_or_none(ctx, (world * R, b))
+    else:  # T(1) on rank 0 alone
+        from paper_2005_09904_b200.sharded import PeerGather
+
+        peer = PeerGather((world * R, b), rank, world, device=dev)
+    y_gather = peer.tensor if peer is not None else torch.empty((world * R, b), device=dev)
     ws = bq.Workspace(int(bq.lib.bqg_biqgemm_sharded_p2p_workspace_bytes(m, n, b, beta, mu, world)), device=dev)
     if hasattr(coll, "register"):
         coll.register(x_dev, y_gather, ws.buf)
     cs = coll.collectives()
 
     def call(i):
+        if peer is None:
+            bq.check(bq.lib.bqg_biqgemm_sharded_f32(tiled[i % copies].data_ptr(), alphas[i % copies].data_ptr(),
+                                                    x_dev.data_ptr(), n, y_gather.data_ptr(), m, n, b, beta, mu, rank,
+                                                    world, C.byref(cs), ws.ptr(), ws.nbytes, stream.cuda_stream))
+            return
         bq.check(bq.lib.bqg_biqgemm_sharded_p2p_f32(tiled[i % copies].data_ptr(), alphas[i % copies].data_ptr(),
                                                     x_dev.data_ptr(), n, C.cast(peer.ptrs, C.c_void_p), m, n, b,
                                                     beta, mu, rank, world, C.byref(cs), ws.ptr(), ws.nbytes,
@@ -819,8 +861,10 @@ def c5_time(ctx, bq, keys, alpha, x, rank, world, coll, K, W):
     stream.synchronize()
     if world > 1:
         ctx.barrier()  # no rank unmaps a peer buffer another rank may still store into
-    peer.close()
-    return e2e, comp, digest
+    fused = peer is not None
+    if peer is not None:
+        peer.close()
+    return e2e, comp, digest, fused
 
 
 class _Solo:
@@ -860,14 +904,15 @@ def c5_strong(ctx, bq, args):
     if ctx.rank == 0:
         solo = NcclComm(0, 1) if bq.lib.bqg_nccl_available() else None  # a 1-rank communicator
         if solo is not None:
-            t1, comp1, digest1 = c5_time(ctx, bq, keys, alpha, x, 0, 1, solo, K, W)
+            t1, comp1, digest1, _ = c5_time(ctx, bq, keys, alpha, x, 0, 1, solo, K, W)
             solo.close()
     ctx.barrier()
     if ctx.world == 1:
         out.update({"t1_ms": t1, "t1_compute_ms": comp1, "t1_gbs": round(kb / (t1 * 1e-3) / 1e9, 1),
                     "y_sha256": digest1})
         return out
-    tN, compN, digestN = c5_time(ctx, bq, keys, alpha, x, ctx.rank, ctx.world, ctx.collectives(), K, W)
+    tN, compN, digestN, fusedN = c5_time(ctx, bq, keys, alpha, x, ctx.rank, ctx.world, ctx.collectives(), K, W)
+    out["y_gather"] = "fused peer stores" if fusedN else "NCCL all-gather (peer mapping unavailable)"
     out.update({"n": ctx.world, "tN_ms": tN, "tN_compute_ms": compN, "t1_ms": t1, "t1_compute_ms": comp1,
                 "tN_gbs": round(kb / (tN * 1e-3) / 1e9, 1)})
     if t1:

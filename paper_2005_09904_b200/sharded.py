@@ -362,13 +362,18 @@ class PeerGather:
         torch.cuda.synchronize(self.tensor.device)
         h = (C.c_char * 64)()
         off = C.c_size_t()
-        _capi.check(lib.bqg_ipc_get_handle(C.c_void_p(self.tensor.data_ptr()), h, C.byref(off)))
-        mine = (bytes(h), off.value)
+        # a rank that cannot export its buffer still takes part in the
+        # exchange (None), so no rank is left waiting in the collective
+        mine = None
+        if lib.bqg_ipc_get_handle(C.c_void_p(self.tensor.data_ptr()), h, C.byref(off)) == 0:
+            mine = (bytes(h), off.value)
         allh = [None] * world
         if world > 1:
             dist.all_gather_object(allh, mine, group=group)
         else:
             allh = [mine]
+        if any(a is None for a in allh):
+            raise RuntimeError("PeerGather: a rank could not export its gather buffer (CUDA IPC)")
         self.opened = []
         ptrs = []
         for r in range(world):
@@ -377,7 +382,11 @@ class PeerGather:
                 continue
             p = C.c_void_p()
             hb, o = allh[r]
-            _capi.check(lib.bqg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb), o, C.byref(p)))
+            st = lib.bqg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb), o, C.byref(p))
+            if st != 0:
+                self.close()
+                msg = lib.bqg_last_error_message().decode(errors="replace")
+                raise RuntimeError(f"PeerGather: rank {r}'s buffer could not be mapped: {msg}")
             self.opened.append(p.value)
             ptrs.append(p.value)
         self.ptrs = (C.c_void_p * world)(*ptrs)

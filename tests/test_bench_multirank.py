@@ -24,8 +24,11 @@ def _port():
 
 
 @pytest.mark.gpu
-def test_bench_two_ranks_one_gpu(cuda):
-    env = dict(os.environ, BQG_BENCH_BACKEND="gloo", BQG_BENCH_ONE_DEVICE="1")
+@pytest.mark.parametrize("no_p2p", ["0", "1"])
+def test_bench_two_ranks_one_gpu(cuda, no_p2p):
+    """no_p2p = 1: the fallback when peer buffers cannot be mapped (the NCCL
+    all-gather entries), chosen collectively."""
+    env = dict(os.environ, BQG_BENCH_BACKEND="gloo", BQG_BENCH_ONE_DEVICE="1", BQG_BENCH_NO_P2P=no_p2p)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3",
            "--warmup", "3", "--no-comparators", "--c5-steps", "2"]
@@ -40,3 +43,4 @@ def test_bench_two_ranks_one_gpu(cuda):
     c5 = d["c5_strong"]
     assert c5["n"] == 2 and c5["tN_ms"] > 0
     assert c5["y_bitwise_equal_to_t1"] is True
+    assert ("NCCL" in d["y_gather"]) == (no_p2p == "1")
