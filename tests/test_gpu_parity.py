@@ -292,11 +292,16 @@ def test_large_mu_fast_path_rekeyed(bq, port, cuda, m, n, beta, mu):
         y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x)
         assert_close(layer.forward(x), y_ref)
         assert np.array_equal(layer.forward(x, exact=True), layer.forward(x, exact=True))
-    # a group of such layers through the grouped host pipeline == one by one
-    xs = np.stack([bq.random_normal(n, 1, 40 + i) for i in range(6)])
-    yg = bq.layers_forward([layer] * 6, xs)
-    for i in range(6):
-        assert np.array_equal(yg[i], layer.forward(xs[i]))
+    # a group of such layers through the grouped host pipeline == one by one,
+    # for x of n rows and of G*mu rows (the whole re-keyed width when it is
+    # wider than 8*ceil(n/8))
+    for rows in sorted({n, G * mu}):
+        xs = np.stack([bq.random_normal(rows, 1, 40 + i) for i in range(6)])
+        yg = bq.layers_forward([layer] * 6, xs)
+        for i in range(6):
+            assert np.array_equal(yg[i], layer.forward(xs[i]))
+        y_ref, _ = port.biqgemm(keys.astype(np.uint32), alpha, n, mu, xs[5])
+        assert_close(yg[5], y_ref)
     layer.close()
 
 
