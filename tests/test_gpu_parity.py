@@ -258,6 +258,19 @@ def test_bqgm_load_forward(bq, ref, cuda):
     assert_close(layer12.forward(x), y12)  # the re-keyed mu = 8 fast path
 
 
+def test_large_mu_random_sweep(cuda):
+    """tools/rand_large_mu.py: random (m, n, beta, mu 9..16, b, x rows up to
+    G*mu) through the re-keyed fast path against the C oracle (rel-Frobenius
+    and max-abs <= 1e-5), grouped host calls bitwise equal to single calls."""
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "tools" / "rand_large_mu.py"), "40"], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "cases ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("m,n,beta,mu", [(300, 500, 2, 12), (1000, 777, 3, 10), (64, 4096, 1, 9), (96, 1000, 2, 16),
                                          (4096, 4096, 3, 10), (33, 13, 2, 11)])
 def test_large_mu_fast_path_rekeyed(bq, port, cuda, m, n, beta, mu):
