@@ -26,6 +26,7 @@
 // fp64 -> fp32; blocks ascending in fp64), so y is bitwise identical to
 // bqg_biqgemm_grouped_f32 and independent of the cluster split.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -66,8 +67,9 @@ constexpr int kLThreads = kLW * 32;
 constexpr int kPieceChunks = BQG_LAT_PIECE;  // chunks (KiB) per key copy
 constexpr int kMaxPieces = 64;
 constexpr int kBarBytes = 1024;  // kbar[kMaxPieces] + abar + pbar
-constexpr uint32_t kLutBase = 0x10000u;
-constexpr int kLatSmem = 227 * 1024;
+constexpr uint32_t kLutBytes = 0x10000u;  // 256 key rows x 256 B (32 tables x 2 blocks x fp32)
+constexpr int kLatSmem = 227 * 1024;      // the most a CTA may ask for
+constexpr int kLatSmemMin = 116 * 1024;   // > half an SM's 228 KiB: one CTA per SM
 
 struct LatArgs {
     int debug;            // BQG_DEBUG_FLAGS & 2: per-CTA globaltimer timeline
@@ -77,6 +79,7 @@ struct LatArgs {
     float* y;
     long long x_rows;
     int m, NB, MT, CS, bpc, tq, tr;
+    int smem;             // dynamic shared memory bytes: LUT + bars/alpha/sums/slots + keys
 };
 
 __device__ __forceinline__ void sts_pair(uint32_t col, int k, float v) {
@@ -134,14 +137,14 @@ __device__ __forceinline__ void build_share(int which, uint32_t col, const float
 }
 
 // ---- gather (identical arithmetic to biqgemm_stream.cu) -------------------
-// base = the CTA's cluster-rank bits (warp-uniform; ptxas keeps it in a
+// base = the LUT's shared address (warp-uniform; ptxas keeps it in a
 // uniform register and folds it into the LDS address: [R + UR + imm]).
 template <int IMM>
 __device__ __forceinline__ float lds_lut(uint32_t rotw, uint32_t w, uint32_t sel, uint32_t base) {
     uint32_t off;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(rotw), "r"(w), "r"(sel));
     float e;
-    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off + base), "n"(kLutBase + IMM));
+    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(e) : "r"(off + base), "n"(IMM));
     return e;
 }
 __device__ __forceinline__ uint64_t pack2(float a, float b) {
@@ -209,27 +212,23 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
     const int npb = (nchunk_b + kPieceChunks - 1) / kPieceChunks;  // key pieces per block
     const int npieces = npb * bpc;
 
-    // ---- shared memory: [bars | alpha | psum | push slots | keys.. | LUT @64K | ..keys]
+    // ---- shared memory: [LUT 64 KiB | bars | alpha | psum | push slots | keys]
+    // sized to what the call needs (A.smem), so that a CTA of the NEXT call of
+    // a PDL chain fits on the same SM (2 x <= 113 KiB) and streams its keys in
+    // while this one computes.  The LUT is at the start of the dynamic window;
+    // the gather addresses it as [PRMT result + LUT base (uniform) + imm].
     const uint32_t sbase = smem_u32(smem);
-    uint64_t* kbar = reinterpret_cast<uint64_t*>(smem);   // [kMaxPieces]
-    uint64_t* abar = kbar + kMaxPieces;                   // alpha landed
-    uint64_t* pbar = abar + 1;                            // pushes into this CTA landed
-    float* as = reinterpret_cast<float*>(smem + kBarBytes);  // [BETA][nt*32]
-    float* psum = as + BETA * nt * 32;                     // [nchunk][32]
-    float* slots = psum + nchunk * 32;                     // [NB][rpo]
+    const uint32_t lut_abs = sbase;
+    uint64_t* kbar = reinterpret_cast<uint64_t*>(smem + kLutBytes);  // [kMaxPieces]
+    uint64_t* abar = kbar + kMaxPieces;                              // alpha landed
+    uint64_t* pbar = abar + 1;                                       // pushes into this CTA landed
+    float* as = reinterpret_cast<float*>(smem + kLutBytes + kBarBytes);  // [BETA][nt*32]
+    float* psum = as + BETA * nt * 32;                                   // [nchunk][32]
+    float* slots = psum + nchunk * 32;                                   // [NB][rpo]
     const uint32_t lo_end = smem_u32(slots + A.NB * rpo);
-    const uint32_t keys_lo = (lo_end + 127u) & ~127u;
-    // Shared addresses of a cluster CTA carry its rank in bits 24.. (rank r's
-    // window starts at r << 24: tools/ubench/smem_base.cu); TMA and DSMEM
-    // addresses keep those bits.  The LUT sits at offset kLutBase of the
-    // CTA's own window; the gather addresses it with the rank-less LDS
-    // immediate (shared::cta accesses resolve within the executing CTA).
-    const uint32_t rank_bits = sbase & 0xFF000000u;
-    const uint32_t lut_abs = rank_bits | kLutBase;
+    const uint32_t keys_at = (lo_end + 127u) & ~127u;
     const uint32_t kbytes = static_cast<uint32_t>(nchunk) * 1024u;
-    // keys go below the LUT if they fit, else above it
-    const uint32_t keys_at = keys_lo + kbytes <= lut_abs ? keys_lo : lut_abs + 0x10000u;
-    if (sbase > lut_abs || lo_end > lut_abs || keys_at + kbytes > sbase + kLatSmem || npieces > kMaxPieces) __trap();
+    if ((sbase & 127u) != 0 || keys_at + kbytes > sbase + static_cast<uint32_t>(A.smem) || npieces > kMaxPieces) __trap();
 
     const uint32_t own_bytes = static_cast<uint32_t>(own1 - own0) * 4u * static_cast<uint32_t>(A.NB);
     if (threadIdx.x == 0) {
@@ -326,7 +325,7 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
         mbar_wait(&kbar[b * npb + c / kPieceChunks], 0);
         if (tl && q == 0) g_timeline_lat[blockIdx.x][10] = gtime();
         const uint32_t ka = keys_at + static_cast<uint32_t>(q) * 1024u;
-        const float P = b == 0 ? gather_chunk_l<0>(ka, lane, rot, rank_bits) : gather_chunk_l<128>(ka, lane, rot, rank_bits);
+        const float P = b == 0 ? gather_chunk_l<0>(ka, lane, rot, lut_abs) : gather_chunk_l<128>(ka, lane, rot, lut_abs);
         psum[q * 32 + lane] = P;
     }
     if (tl) {
@@ -395,7 +394,7 @@ cudaError_t launch_lat_beta(const LatArgs& A, int nclusters, bool pdl, cudaStrea
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(nclusters * A.CS));
     cfg.blockDim = dim3(kLThreads);
-    cfg.dynamicSmemBytes = kLatSmem;
+    cfg.dynamicSmemBytes = static_cast<size_t>(A.smem);
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
@@ -496,15 +495,25 @@ bool plan_latency(const QueryParams& p, LatArgs& A, int& nclusters) {
     nclusters = std::min(best_n, A.MT);
     A.tq = A.MT / nclusters;
     A.tr = A.MT % nclusters;
-    // shared-memory fit of the largest cluster range (keys, alpha, sums, slots)
+    // shared memory of the largest cluster range: LUT, bars, alpha, sums, slots, keys
     {
         const long long nt = A.tq + (A.tr ? 1 : 0);
         const long long lo = kBarBytes + 4 * nt * 32 * p.beta + 4 * nt * 32 * p.beta * A.bpc +
                              4LL * A.NB * ((nt * 32 + A.CS - 1) / A.CS);
         const long long keys = nt * p.beta * A.bpc * 1024;
-        const bool fits = lo + 1024 <= 0x10000 - 1024 && (lo + keys + 1024 <= 0x10000 - 1024 || 0x20000 + keys <= kLatSmem) &&
-                          (nt * p.beta + kPieceChunks - 1) / kPieceChunks * A.bpc <= kMaxPieces;
-        if (!fits) return false;
+        const long long need = (static_cast<long long>(kLutBytes) + lo + 128 + keys + 1023) / 1024 * 1024;
+        if (need > kLatSmem || (nt * p.beta + kPieceChunks - 1) / kPieceChunks * A.bpc > kMaxPieces) return false;
+        // At least kLatSmemMin: one CTA per SM.  A second CTA on the SM (a
+        // smaller request) was measured SLOWER (beta = 1: 4.87 vs 4.04 us per
+        // dependent call, beta = 2: 6.29 vs 4.97): the cluster scheduler then
+        // packs a call's own CTAs two per SM.  Asking for less than the
+        // whole 227 KiB leaves L1 for x and the alpha rows (BQG_LAT_SMEM=full:
+        // the old 227 KiB request, for A/B).
+        static const bool full = [] {
+            const char* e = getenv("BQG_LAT_SMEM");
+            return e && e[0] == 'f';
+        }();
+        A.smem = full ? kLatSmem : static_cast<int>(std::max<long long>(need, kLatSmemMin));
     }
     return true;
 }
