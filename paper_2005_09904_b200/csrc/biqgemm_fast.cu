@@ -144,6 +144,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, BT == 1 ? 2 : 1)
                     const int cnt = min(TPS, seg_end - pbase - t0);
                     const int slot = sc % R;
                     mbar_wait(&empty[slot], ((sc / R) & 1) ^ 1);
+                    // Stage 0 lands ALONE before the rest of the fill is
+                    // requested: every CTA asking for its whole ring at once
+                    // (up to 20 MB in flight) delayed the first stage to
+                    // ~3 us (C4 b = 2: 13.6 -> 12.9 us per call; BQG_DEBUG_FLAGS
+                    // bit 21 restores the old order for A/B)
+                    if (sc == 1 && !(p.debug & (1 << 21))) mbar_wait(&full[0], 0);
                     mbar_arrive_expect_tx(&full[slot], cnt * TILE_BYTES);
                     bulk_g2s(stages + static_cast<size_t>(slot) * STAGE_BYTES, kpair + static_cast<long long>(t0) * TILE_BYTES,
                              cnt * TILE_BYTES, &full[slot], pol);
@@ -364,7 +370,15 @@ bool ring_shape(int mu, int bt, int beta, FastPlan& pl) {
         const int tps = static_cast<int>(std::min<size_t>(kNW, avail / (kMinStages * tile)));
         if (tps < 1) continue;
         pl.tps = tps;
-        pl.R = static_cast<int>(std::min<size_t>(6, avail / (tps * tile)));
+        // ring depth: 2 stages for BT = 4 (C3 25.66 -> 25.42, C5 147.9 ->
+        // 147.4 us; b = 4..64 neutral), up to 6 otherwise (BT = 2: C4 b = 2
+        // 13.0 at 2 vs 12.9 at 6); BQG_FAST_RMAX overrides (A/B knob)
+        static const int rmax_env = [] {
+            const char* e = getenv("BQG_FAST_RMAX");
+            return e ? std::max(2, atoi(e)) : 0;
+        }();
+        const int rmax = rmax_env ? rmax_env : (bt == 4 ? 2 : 6);
+        pl.R = static_cast<int>(std::min<size_t>(rmax, avail / (tps * tile)));
         return true;
     }
     return false;
