@@ -131,6 +131,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                     const int cnt = min(NW, cps - c0);
                     const int slot = sc % R;
                     if (sc >= R) mbar_wait(&empty[slot], ((sc / R) & 1) ^ 1);  // first R stages are free
+                    // stage 0 lands alone before the rest of the fill is requested
+                    // (C2 b = 2 7.94 -> 7.82 us, b = 3 / 4 neutral; bit 21: old order)
+                    if (sc == 1 && !(p.debug & (1 << 21))) mbar_wait(&full[0], 0);
                     if ((p.debug & 2) && blockIdx.x < 8192 && sc == 0) g_timeline_c[blockIdx.x][13] = gtimer_c();
                     mbar_arrive_expect_tx(&full[slot], cnt * 1024);
                     bulk_g2s(stages + slot * STAGE_BYTES, kseg + static_cast<long long>(c0) * 1024, cnt * 1024,
