@@ -79,7 +79,12 @@ def main():
          "(`--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none`; "
          "cold-cache and serialised: compare shares, not absolutes).", ""]
     for cfg in cfgs:
-        m, n, beta, b, mu = CONFIGS[cfg]
+        if cfg in CONFIGS:
+            m, n, beta, b, mu = CONFIGS[cfg]
+        else:  # e.g. C4b2: a config with its batch overridden
+            base, bb = cfg.split("b", 1)
+            m, n, beta, b, mu = CONFIGS[base]
+            b = int(bb)
         kb = key_bytes(m, n, beta, mu)
         for rep, kname, calls in ((d / f"full_{cfg}.ncu-rep", "biqgemm_stream_kernel", 128),
                                   (d / f"full_tex_{cfg}.ncu-rep", "biqgemm_tex_kernel", 128),
