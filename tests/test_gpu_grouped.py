@@ -175,7 +175,10 @@ def test_layers_forward_host_pipeline(bq, port, cuda):
 
 
 @pytest.mark.parametrize("m,n,beta", [(1, 8, 1), (33, 7, 2), (100, 300, 3), (1000, 777, 4), (4096, 4096, 3),
-                                      (2000, 4096, 1), (16384, 4096, 3), (70, 2048, 2), (5000, 1024, 3)])
+                                      (2000, 4096, 1), (16384, 4096, 3), (70, 2048, 2), (5000, 1024, 3),
+                                      # larger m: the stream form's group of one
+                                      (12000, 4096, 1), (20000, 4096, 2), (16384, 4096, 4), (30000, 2048, 3),
+                                      (9000, 4096, 4), (16400, 3000, 3)])
 def test_single_call_latency_form_matches_stream_form(bq, port, cuda, m, n, beta):
     """The single-call latency kernel (b == 1, mu == 8) uses the stream form's
     arithmetic: y is bitwise identical to a grouped call of one, and within
@@ -312,3 +315,44 @@ def test_layers_forward_host_graph_replay(bq, port, cuda):
     assert_close(y_pin[5].numpy(), port.biqgemm(keys.astype(np.uint32), alpha, n, mu, x_pin[5].numpy())[0])
     for L in layers2:
         L.close()
+
+
+@pytest.mark.parametrize("m,n,beta", [(16384, 4096, 3), (20000, 4096, 2), (4096, 4096, 3)])
+def test_dependent_chain_pdl_graph_bitwise(bq, cuda, m, n, beta):
+    """A PDL-chained CUDA graph of single calls, each x = the previous call's
+    y (square layers) or a fixed x, gives the same y as the calls run one by
+    one without PDL -- covers the latency form's key ring (C4-sized layers)
+    across launches that overlap their prologues."""
+    import torch
+
+    rng = np.random.default_rng(5 + m)
+    G = (n + 7) // 8
+    K = 12
+    tiles = [bq.tile_keys(torch.from_numpy(rng.integers(0, 256, size=(beta, m, G), dtype=np.uint8)).cuda(), n, 8)
+             for _ in range(3)]
+    # alpha ~ 1/(n beta): a chained y stays finite over K layers
+    al = torch.from_numpy(rng.uniform(0.5, 1.5, size=(beta, m)).astype(np.float32) / (n * beta)).cuda()
+    chain = m == n
+    x0 = torch.from_numpy(bq.random_normal(n, 1, 3)).cuda()
+    ws = bq.Workspace(int(bq.lib.bqg_biqgemm_workspace_bytes(m, n, 1, beta, 8)))
+
+    def run(pdl, stream, ys):
+        for i in range(K):
+            x = ys[i - 1] if (chain and i > 0) else x0
+            bq.biqgemm_device(tiles[i % 3], al, x, ys[i], m, n, beta, 8, ws, pdl=pdl, stream=stream)
+
+    ref = [torch.empty((m, 1), device="cuda") for _ in range(K)]
+    run(False, None, ref)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    out = [torch.full((m, 1), float("nan"), device="cuda") for _ in range(K)]
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            run(True, s.cuda_stream, out)
+        for _ in range(3):
+            g.replay()
+    s.synchronize()
+    for a, b in zip(ref, out):
+        assert bool(torch.isfinite(a).all())
+        assert torch.equal(a, b)
