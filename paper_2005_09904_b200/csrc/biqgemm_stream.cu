@@ -312,15 +312,8 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
         if (lane < nst) {
             const uint64_t pol = policy_evict_first();
             const long long nstages_total = static_cast<long long>(ncalls) * spc;
-            for (long long s = lane; s < nstages_total; s += nst) {
-                const int slot = lane;
-                const long long round = s / nst;
-                if (round > 0) mbar_wait_sleep(&empty[slot], static_cast<uint32_t>((round - 1) & 1));
-                // stage 0 lands ALONE before the other lanes request theirs:
-                // a whole-ring request from every CTA delays the first stage
-                // (C4 single call 12.67 -> 12.10 us, C2 group of one 6.68 ->
-                // 6.24; BQG_DEBUG_FLAGS bit 21 restores the old order)
-                else if (lane != 0 && !(A.debug & (1 << 21))) mbar_wait(&full[0], 0);
+            const int slot = lane;
+            auto issue = [&](long long s) {
                 const int c = static_cast<int>(s / spc), j = static_cast<int>(s - static_cast<long long>(c) * spc);
                 const int k0 = j * A.ups, len = min(A.ups, U - k0);
                 const uint32_t bytes = static_cast<uint32_t>(len) * BETA * 1024u;
@@ -332,6 +325,24 @@ __global__ void __launch_bounds__(kSThreads, 1) biqgemm_stream_kernel(const __gr
                     : "memory");
                 // issued[slot] = round + 1 (one increment per round), as an atomic
                 asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&issued[slot])) : "memory");
+            };
+            long long s0 = lane;
+            // Stage 0 lands ALONE before the other lanes request theirs: a
+            // whole-ring request from every CTA delays the first stage (C4
+            // single call 12.67 -> 12.06 us, C2 group of one 6.68 -> 6.24;
+            // BQG_DEBUG_FLAGS bit 21 restores the old order).  Every issuing
+            // lane sees phase 0 of slot 0 before lane 0 can refill the slot
+            // (the __syncwarp), so no lane tests a later phase of the same parity.
+            if (nstages_total > 1 && !(A.debug & (1 << 21))) {
+                if (lane == 0) issue(0);
+                mbar_wait(&full[0], 0);
+                __syncwarp(nst >= 32 ? 0xffffffffu : ((1u << nst) - 1u));
+                if (lane == 0) s0 = nst;
+            }
+            for (long long s = s0; s < nstages_total; s += nst) {
+                const long long round = s / nst;
+                if (round > 0) mbar_wait_sleep(&empty[slot], static_cast<uint32_t>((round - 1) & 1));
+                issue(s);
             }
         }
         return;
