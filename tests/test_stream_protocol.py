@@ -46,3 +46,14 @@ def test_model_catches_the_unguarded_ring():
     finally:
         sim.make = orig
     assert bad > 0
+
+
+@pytest.mark.parametrize("stagger", [True, False])
+def test_ring_start_orders(stagger):
+    """Both ring starts are deadlock-free: stage 0 alone first (the kernel's
+    default) and the whole ring at once (BQG_DEBUG_FLAGS bit 21)."""
+    for U, ups, nst in ((1, 6, 2), (15, 4, 6), (57, 4, 9), (40, 6, 12)):
+        for ncalls in (1, 2, 5):
+            for seed in range(3):
+                assert sim.run(ncalls, U, ups, nst, 18, 4, 2, seed=seed, stagger=stagger) is None
+

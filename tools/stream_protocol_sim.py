@@ -31,12 +31,14 @@ class Bar:
         return (self.phase & 1) != parity
 
 
-def make(ncalls, U, ups, nst, nc, nlb, nab=2, nbuild=4):
+def make(ncalls, U, ups, nst, nc, nlb, nab=2, nbuild=4, stagger=True):
     """Roles and barriers of biqgemm_stream_kernel: key warp lanes (one ring
     slot each, ungated, publishing issued[]), x loader (4 buffers), alpha
     loader (nab buffers), nbuild LUT builders (nlb buffers), nc gather warps
     (continuous unit assignment, call-aligned stages, count-completing
-    arrival on a partial stage)."""
+    arrival on a partial stage).  stagger: the kernel's ring start -- lane 0
+    issues stage 0 alone, every issuing lane waits for its landing, then a
+    __syncwarp of the issuing lanes (psync) before lane 0 may refill slot 0."""
     spc = (U + ups - 1) // ups
     B = {}
     for i in range(nst):
@@ -50,8 +52,19 @@ def make(ncalls, U, ups, nst, nc, nlb, nab=2, nbuild=4):
         B[("afull", i)] = Bar(1)
         B[("adone", i)] = Bar(nc)
 
+    B[("psync",)] = Bar(nst)
+
     def producer(L):
         s = L
+        if stagger and ncalls * spc > 1:
+            if L == 0:
+                yield ("set", ("issued", 0), 1)
+                yield ("arrive", ("full", 0), 1)
+            yield ("wait", ("full", 0), 0, 0)
+            yield ("arrive", ("psync",), 1)
+            yield ("wait", ("psync",), 0, 0)
+            if L == 0:
+                s = nst
         while s < ncalls * spc:
             rnd = s // nst
             if rnd > 0:
@@ -104,10 +117,10 @@ def make(ncalls, U, ups, nst, nc, nlb, nab=2, nbuild=4):
     return B, procs
 
 
-def run(ncalls, U, ups, nst, nc, nlb, nab=2, seed=0):
+def run(ncalls, U, ups, nst, nc, nlb, nab=2, seed=0, stagger=True):
     """Returns None if every role finishes, else a description of the failure."""
     rng = random.Random(seed)
-    B, procs = make(ncalls, U, ups, nst, nc, nlb, nab)
+    B, procs = make(ncalls, U, ups, nst, nc, nlb, nab, stagger=stagger)
     cur = [next(p, None) for p in procs]
     cnt = {}
     while True:
