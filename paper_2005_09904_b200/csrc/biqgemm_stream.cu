@@ -42,6 +42,7 @@
 // independent of the grid, the group size and any 32-row-aligned row
 // sharding.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -580,6 +581,16 @@ size_t stream_workspace_bytes(long long m, long long groups, int count) {
     return kTexCounterBytes + static_cast<size_t>(per * NB * MT * 32) * sizeof(float);
 }
 
+int tex_min_group(long long m) {
+    // Crossovers measured after the ring-start change (per call, PDL-chained
+    // grouped launches, `profiles/ab_grouped_crossover_r2e.txt`): ~9 calls at
+    // m = 4096 (beta 1 and 3), 13-16 at m = 8192-11008, 16-24 at 16384 -- the
+    // texture form's fixed cost (the last calls' finalisation, one CTA per
+    // call) grows with m.  9 * sqrt(m / 4096), at least kTexMinGroup.
+    const double t = 9.0 * std::sqrt(static_cast<double>(m) / 4096.0);
+    return std::max(kTexMinGroup, static_cast<int>(std::lround(t)));
+}
+
 cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long x_rows, int m, int G, int beta,
                                   float* ws, bool pdl, cudaStream_t stream) {
     static const int impl = [] {
@@ -589,7 +600,7 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
     // The texture form finalises in-kernel (the last CTA to finish a call sums
     // its partials), which pays off over a group; a call or two alone keeps
     // this TMA-ring form, whose finaliser is a separate wide kernel.
-    if (impl == 0 && count >= kTexMinGroup && tex_stream_applies(m, G, beta))
+    if (impl == 0 && count >= tex_min_group(m) && tex_stream_applies(m, G, beta))
         return launch_biqgemm_tex(calls, count, x_rows, m, G, beta, ws, pdl, stream);
     const int sms = device_sms(current_device());
     StreamArgs A{};

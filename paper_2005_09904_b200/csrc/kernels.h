@@ -76,7 +76,13 @@ cudaError_t launch_biqgemm_stream(const StreamCall* calls, int count, long long 
 // pipe (biqgemm_tex.cu); launch_biqgemm_stream dispatches to it when
 // tex_stream_applies (texel range) unless BQG_STREAM_IMPL=tma.
 bool tex_stream_applies(long long m, int G, int beta);
-constexpr int kTexMinGroup = 4;
+#ifndef BQG_TEX_MIN_GROUP
+#define BQG_TEX_MIN_GROUP 4
+#endif
+constexpr int kTexMinGroup = BQG_TEX_MIN_GROUP;  // smaller groups take the TMA-ring form
+// The group size from which the texture form beats the TMA-ring form for
+// m rows (>= kTexMinGroup; measured crossovers, tools/ab_tex_min_group3.sh).
+int tex_min_group(long long m);
 // peer_base / npeer (<= kMaxPeers): the finaliser also stores every y row at
 // the same offset from local_base in each peer gather buffer (fused
 // all-gather over NVLink; npeer = 0: local y only).

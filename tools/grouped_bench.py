@@ -1,5 +1,5 @@
 """Throughput of the grouped (stream) form vs the single-call PDL chain.
-python tools/grouped_bench.py [C2|C4] [group]"""
+python tools/grouped_bench.py [C2|C4] [group] [m n beta]"""
 import sys
 import time
 from pathlib import Path
@@ -14,6 +14,8 @@ from bench import CONFIGS, SEED, L2_BYTES, key_bytes  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 group = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 m, n, beta, b, mu = CONFIGS[cfg]
+if len(sys.argv) > 5:  # shape override: python tools/grouped_bench.py C2 G m n beta
+    m, n, beta = int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
 kb = key_bytes(m, n, beta, mu)
 layer = bq.PackedLinear.from_weights(bq.random_uniform(m, n, SEED), beta, mu)
 keys, alpha = layer.export()
