@@ -213,10 +213,9 @@ __global__ void __launch_bounds__(kLThreads, 1) biqgemm_latency_kernel(const __g
     const int npieces = npb * bpc;
 
     // ---- shared memory: [LUT 64 KiB | bars | alpha | psum | push slots | keys]
-    // sized to what the call needs (A.smem), so that a CTA of the NEXT call of
-    // a PDL chain fits on the same SM (2 x <= 113 KiB) and streams its keys in
-    // while this one computes.  The LUT is at the start of the dynamic window;
-    // the gather addresses it as [PRMT result + LUT base (uniform) + imm].
+    // sized to what the call needs (A.smem, at least kLatSmemMin: one CTA per
+    // SM).  The LUT is at the start of the dynamic window; the gather
+    // addresses it as [PRMT result + LUT base (uniform) + imm].
     const uint32_t sbase = smem_u32(smem);
     const uint32_t lut_abs = sbase;
     uint64_t* kbar = reinterpret_cast<uint64_t*>(smem + kLutBytes);  // [kMaxPieces]
