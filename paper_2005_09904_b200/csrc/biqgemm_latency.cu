@@ -432,8 +432,11 @@ int max_clusters(int cs) {
 
 }  // namespace
 
+// NB group blocks split over a cluster of CS CTAs, NB / CS = 1 or 2 blocks each
+// (CS <= 16: NB <= 16, i.e. n <= 4096 at mu = 8; any NB -- clusters of 3, 5,
+// 6, 7, ... CTAs included, e.g. n = 3072: NB = 12, clusters of 6 or 12)
 bool latency_supported(int mu, int beta, long long b, int NB) {
-    return mu == kMU && b == 1 && beta >= 1 && beta <= 4 && (NB == 1 || NB == 2 || NB == 4 || NB == 8 || NB == 16);
+    return mu == kMU && b == 1 && beta >= 1 && beta <= 4 && NB >= 1 && NB <= 16;
 }
 
 namespace {
@@ -474,7 +477,7 @@ bool plan_latency(const QueryParams& p, LatArgs& A, int& nclusters) {
     A.MT = p.MT;
     // cluster of CS CTAs x bpc blocks per CTA: the shape that covers the most SMs
     int best_cs = 0, best_n = 0;
-    for (int cs : {16, 8, 4, 2, 1}) {
+    for (int cs = 16; cs >= 1; --cs) {
         if (cs > A.NB || A.NB % cs != 0 || A.NB / cs > 2) continue;
         int n = 0;
         switch (p.beta) {

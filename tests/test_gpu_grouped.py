@@ -178,7 +178,10 @@ def test_layers_forward_host_pipeline(bq, port, cuda):
                                       (2000, 4096, 1), (16384, 4096, 3), (70, 2048, 2), (5000, 1024, 3),
                                       # larger m: the stream form's group of one
                                       (12000, 4096, 1), (20000, 4096, 2), (16384, 4096, 4), (30000, 2048, 3),
-                                      (9000, 4096, 4), (16400, 3000, 3)])
+                                      (9000, 4096, 4), (16400, 3000, 3),
+                                      # latency form with clusters of 3 / 5 / 6 / 7 / 12 CTAs (NB not a power of 2)
+                                      (4096, 3072, 3), (2048, 1536, 2), (3000, 2400, 1), (5000, 1280, 4),
+                                      (1500, 1792, 3), (777, 700, 2)])
 def test_single_call_latency_form_matches_stream_form(bq, port, cuda, m, n, beta):
     """The single-call latency kernel (b == 1, mu == 8) uses the stream form's
     arithmetic: y is bitwise identical to a grouped call of one, and within
