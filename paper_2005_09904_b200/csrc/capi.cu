@@ -801,8 +801,17 @@ int layer_alloc(size_t m, size_t n, unsigned beta, unsigned mu, bool plane_mode,
     L->beta = beta;
     L->mu = mu;
     L->G = groups_of(n, mu);
-    L->fn = mu <= 8 ? n : bqg_rekey_mu8_columns(n, mu);
-    L->fmu = mu <= 8 ? mu : 8;
+    // mu != 8: the same sign bits re-keyed to mu = 8 (mu > 8: u16 keys the
+    // fast kernels do not take; mu < 8: the mu = 8 forms -- latency, texture,
+    // stream -- are several times faster than the mu < 8 two-kernel form;
+    // BQG_REKEY_SMALL_MU=0 keeps mu < 8 layers on their own keys, for A/B)
+    static const bool keep_small_mu = [] {
+        const char* v = getenv("BQG_REKEY_SMALL_MU");
+        return v && v[0] == '0';
+    }();
+    const bool native = mu == 8 || (mu < 8 && keep_small_mu);
+    L->fn = native ? n : bqg_rekey_mu8_columns(n, mu);
+    L->fmu = native ? mu : 8;
     L->plane_mode = plane_mode;
     cudaError_t e = cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&L->d_keys, L->key_bytes_per_plane() * beta);
@@ -819,13 +828,13 @@ int layer_alloc(size_t m, size_t n, unsigned beta, unsigned mu, bool plane_mode,
 }
 
 int layer_finish_tiling(bqg_layer* L) {
-    if (L->mu <= 8) {
+    if (L->fmu == L->mu) {
         cudaError_t e = bqg::launch_tile_keys(static_cast<const uint8_t*>(L->d_keys), static_cast<long long>(L->m),
                                               static_cast<long long>(L->G), static_cast<int>(L->beta), L->d_tiled,
                                               L->stream);
         if (e != cudaSuccess) return cuda_err(e, "tile_keys kernel");
     } else {
-        // mu > 8: the same sign bits as mu = 8 keys, then the fast path's tiling
+        // mu != 8: the same sign bits as mu = 8 keys, then the fast path's tiling
         uint8_t* k8 = nullptr;
         const size_t g8 = L->fn / 8;
         BQG_CUDA(cudaMalloc(reinterpret_cast<void**>(&k8), size_t(L->beta) * L->m * g8));
@@ -1017,7 +1026,7 @@ namespace {
 // covering n keeps the group blocks a mu = 8 layer of n columns has (C2:
 // 16, the latency form's shape) instead of one more nearly empty block.
 size_t fast_columns(const bqg_layer* L, size_t x_rows) {
-    if (L->mu <= 8) return L->n;
+    if (L->fmu == L->mu) return L->n;
     const size_t n8 = 8 * ((L->n + 7) / 8);
     return x_rows <= n8 ? n8 : L->fn;
 }

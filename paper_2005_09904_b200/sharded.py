@@ -224,10 +224,17 @@ class ShardedLinear:
         self.bq = bq
         self.layer = shard_layer  # PackedLinear of rows [lo, hi) (None when the rank owns no rows)
         self.m, self.n, self.beta, self.mu = m, n, beta, mu
-        # the kernels' view: mu > 8 layers run the fast path on their sign bits
-        # re-keyed to mu = 8 (bqg_rekey_mu8; the layer's tiled keys) over
+        # the kernels' view: mu != 8 layers run the fast path on their sign
+        # bits re-keyed to mu = 8 (bqg_rekey_mu8; the layer's tiled keys) over
         # 8*ceil(n/8) columns -- x may have up to that many rows
-        self.kn, self.kmu = (n, mu) if mu <= 8 else (8 * ((n + 7) // 8), 8)
+        nf, mf = C.c_size_t(), C.c_uint()
+        if shard_layer is not None:  # the layer's own fast view
+            bq.check(bq.lib.bqg_layer_fast_shape(shard_layer._h, C.byref(nf), C.byref(mf)))
+            native = mf.value == mu
+        else:  # the rule the library applies (capi.cu: layer creation)
+            import os
+            native = mu == 8 or (mu < 8 and os.environ.get("BQG_REKEY_SMALL_MU", "1")[:1] == "0")
+        self.kn, self.kmu = (n, mu) if native else (8 * ((n + 7) // 8), 8)
         self.rank, self.world = rank, world
         self.plan = ShardPlan.make(m, world)
         self.coll_provider = collectives

@@ -272,7 +272,10 @@ def test_large_mu_random_sweep(cuda):
 
 
 @pytest.mark.parametrize("m,n,beta,mu", [(300, 500, 2, 12), (1000, 777, 3, 10), (64, 4096, 1, 9), (96, 1000, 2, 16),
-                                         (4096, 4096, 3, 10), (33, 13, 2, 11)])
+                                         (4096, 4096, 3, 10), (33, 13, 2, 11),
+                                         # mu < 8 layers are re-keyed to mu = 8 too
+                                         (300, 500, 2, 4), (1000, 777, 3, 6), (64, 4096, 1, 1), (96, 1000, 2, 7),
+                                         (4096, 4096, 3, 5), (33, 13, 2, 3), (2000, 3000, 4, 2)])
 def test_large_mu_fast_path_rekeyed(bq, port, cuda, m, n, beta, mu):
     """mu > 8 on the fast path: the sign bits re-keyed to mu = 8 over
     8*ceil(G*mu/8) columns run the mu <= 8 kernels.  y within the fp32
