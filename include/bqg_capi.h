@@ -125,7 +125,7 @@ int bqg_pack_keys(const uint32_t* d_plane, size_t m, size_t n, unsigned mu, void
 int bqg_tile_keys(const uint8_t* d_keys, size_t m, size_t n, unsigned beta, unsigned mu,
                   uint8_t* d_tiled, void* stream);
 
-/* mu > 8 on the fast path: the sign bits of mu-bit keys (beta x m x G, u16
+/* mu != 8 on the fast path: the sign bits of mu-bit keys (beta x m x G, u16
  * for mu > 8, u8 otherwise) re-keyed as mu = 8 keys over
  * bqg_rekey_mu8_columns(n, mu) = 8*ceil(G*mu/8) columns (beta x m x that/8
  * bytes, row-major; bits past G*mu are 0, like the keys' own pad bits).
@@ -287,11 +287,12 @@ void bqg_layer_destroy(bqg_layer* layer);
 int bqg_layer_shape(const bqg_layer* layer, size_t* m, size_t* n, unsigned* beta, unsigned* mu);
 /* Download keys (row-major, u8/u16) and alpha; plane words too if non-NULL. */
 int bqg_layer_export(const bqg_layer* layer, void* h_keys, float* h_alpha, uint32_t* h_planes);
-/* The fast path's view of a layer: (n, mu) for mu <= 8; for mu > 8 the
- * re-keyed (bqg_rekey_mu8_columns(n, mu), 8) -- the shape its tiled keys
- * have.  A call whose x has at most 8*ceil(n/8) rows runs with that many
- * columns (a prefix of the tiled layout: group blocks are its outer index),
- * so a mu > 8 layer of n columns takes the forms a mu = 8 layer takes. */
+/* The fast path's view of a layer: (n, 8) for mu = 8; for every other mu
+ * the re-keyed (bqg_rekey_mu8_columns(n, mu), 8) -- the shape its tiled keys
+ * have (environment BQG_REKEY_SMALL_MU=0 at layer creation keeps mu < 8
+ * layers on (n, mu)).  A call whose x has at most 8*ceil(n/8) rows runs with
+ * that many columns (a prefix of the tiled layout: group blocks are its outer
+ * index), so a mu != 8 layer of n columns takes the forms a mu = 8 layer takes. */
 int bqg_layer_fast_shape(const bqg_layer* layer, size_t* n_fast, unsigned* mu_fast);
 /* Device views (for device-resident timing and the sharded driver); the
  * tiled keys are in the fast view (bqg_layer_fast_shape). */
